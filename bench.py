@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark: LSTM forward seqs/s and p50 latency on B200, with roofline and
+host-CPU baseline (BASELINE.json metric).
+
+Workload (N=1 line): config c2 — 2-layer LSTM, hidden 1024, seq 128, batch 64,
+fp32 semantics (max-abs 1e-4 vs the float64 oracle), random-init weights,
+synthetic inputs.  One step = one forward of the whole layers x timesteps DAG
+over one batch.  N GPUs = N independent request shards (batch 64 each, weak
+scaling, no collective — the path shards only over independent requests).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W untimed warm-up steps, then exactly K timed steps bracketed by a
+barrier + cuda synchronize; L2 is flushed (256 MiB write) before every timed
+step, outside the per-step CUDA events; device time = sum of per-step event
+durations; the max over ranks is reported.  `e2e` repeats the K steps through
+the public request API with pinned host buffers (H2D of x, D2H of y/h_n/c_n
+inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LSTM seqs/sec and p50 latency (ms) at 1/2/4/8 B200 vs host-CPU ref; % roofline"
+UNIT = "seqs/s"
+CONFIG_NAME = "c2"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        exe = shutil.which("nvidia-smi")
+        if exe:
+            self.proc = subprocess.Popen(
+                [exe, f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_info():
+    import torch
+
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model,
+            "torch_threads": torch.get_num_threads()}
+
+
+def oracle_forward_sample(spec, weights, x):
+    """One float64 oracle forward (the reference-arm / cpu_baseline unit)."""
+    from oracle.rnn_ref import rnn_forward_ref
+
+    return rnn_forward_ref(spec.cell, x, weights, dirs=spec.dirs)
+
+
+def cpu_sample_setup(spec, sample_batch):
+    from paper_2307_11339_b200 import init_weights, make_input
+
+    w = [{k: v.double().numpy() for k, v in d.items()} for d in init_weights(spec, 0)]
+    x = make_input(spec, 1)[:, :sample_batch].double().numpy().copy()
+    return w, x
+
+
+def time_cpu_baseline(spec, budget_s: float, sample_batch: int):
+    """Oracle port on the host cores, bounded to ~budget_s seconds."""
+    w, x = cpu_sample_setup(spec, sample_batch)
+    t0 = time.perf_counter()
+    oracle_forward_sample(spec, w, x)  # warm (BLAS thread pool)
+    first = time.perf_counter() - t0
+    reps = max(1, min(20, int(budget_s / max(first, 1e-3))))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle_forward_sample(spec, w, x)
+        times.append(time.perf_counter() - t0)
+    p50 = statistics.median(times)
+    return {"value": sample_batch / p50, "unit": UNIT, "p50_ms": p50 * 1e3, "reps": reps,
+            "sample": f"{CONFIG_NAME} forward on {sample_batch} of {spec.batch} sequences (full T={spec.seq}, L={spec.layers}), float64 numpy oracle, median of {reps}"}
+
+
+def torch_cpu_reference(spec, sample_batch, reps=3):
+    """Fused torch.nn.LSTM fp32 on the host (best-case CPU path, context only)."""
+    import torch
+
+    from paper_2307_11339_b200 import init_weights, make_input
+
+    m = torch.nn.LSTM(spec.I, spec.hidden, spec.layers) if spec.cell == "lstm" else torch.nn.GRU(spec.I, spec.hidden, spec.layers)
+    x = make_input(spec, 1)[:, :sample_batch].contiguous()
+    with torch.no_grad():
+        m(x)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            m(x)
+            ts.append(time.perf_counter() - t0)
+    p50 = statistics.median(ts)
+    return {"value": sample_batch / p50, "p50_ms": p50 * 1e3, "threads": torch.get_num_threads()}
+
+
+def run_reference(args, spec):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+
+    info = cpu_info()
+    sample_batch = args.ref_sample_batch
+    w, x = cpu_sample_setup(spec, sample_batch)
+    for _ in range(args.warmup):
+        oracle_forward_sample(spec, w, x)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_forward_sample(spec, w, x)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = sample_batch * args.steps / total
+    p50 = statistics.median(times) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "p50_ms": p50,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{CONFIG_NAME}: 2-layer LSTM H1024 T128, forward; reference-arm step = {sample_batch}-sequence sample",
+                   "batch_per_gpu": spec.batch, "sample_batch": sample_batch},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["affinity"], "kind": "port",
+                         "sample": f"float64 numpy oracle (oracle/rnn_ref.py) cell DAG forward on {sample_batch} sequences, all host threads via BLAS",
+                         "host": info},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default=CONFIG_NAME)
+    ap.add_argument("--algo", default="auto")
+    ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-sample-batch", type=int, default=64)
+    ap.add_argument("--ref-sample-batch", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    from paper_2307_11339_b200.rnn import CONFIGS
+
+    spec = CONFIGS[args.config].with_(algo=args.algo)
+    if args.impl == "reference":
+        return run_reference(args, spec)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device(f"cuda:{local if world > 1 else 0}")
+
+    from paper_2307_11339_b200 import init_weights, make_input
+    from paper_2307_11339_b200.rnn import RNNExecutor
+    from paper_2307_11339_b200.serve import InferenceRequest, RNNServer
+
+    weights = init_weights(spec, 0)
+    ex = RNNExecutor(spec, weights, device=dev)
+    x_host = make_input(spec, 1 + rank).pin_memory()
+    x = x_host.to(dev)
+    outs = ex.alloc_outputs()
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        ex.forward(x, out=outs)
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed region: exactly K steps
+    step_ms, layer_ms = [], []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clocks:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            *_, lm = ex.forward(x, out=outs, layer_ms=True)
+            evs[i][1].record(stream)
+            layer_ms.append(lm)
+        torch.cuda.synchronize(dev)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = max_over_ranks(sum(step_ms))
+
+    # ---- end-to-end through the public request API (pinned host buffers)
+    server = RNNServer(ex)
+    req = InferenceRequest(x=x_host)
+    for _ in range(2):
+        server.run(req)
+    e2e_ms = []
+    barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        resp = server.run(req)
+        e2e_ms.append(resp.device_ms)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_total = max_over_ranks(sum(e2e_ms))
+    h2d = resp.h2d_bytes
+    d2h = resp.d2h_bytes
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    B_total = spec.batch * world
+    value = B_total * args.steps / (total_ms / 1e3)
+    p50 = statistics.median(step_ms)
+    p90 = sorted(step_ms)[int(0.9 * (len(step_ms) - 1))]
+    gemm_f, rec_f = spec.flops()
+    rec_ms = statistics.mean(sum(l[1] for l in lm) for lm in layer_ms)  # all layers, per forward
+    gemm_ms = statistics.mean(sum(l[0] for l in lm) for lm in layer_ms)
+    peaks = load_peaks()
+    achieved = rec_f / (rec_ms / 1e3) / 1e12
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        tdoc = json.loads(tfile.read_text())
+        traffic = tdoc.get(f"{CONFIG_NAME}:{ex.algo}:recurrent")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": p90,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if spec.dtype == "f32" else "bf16", "data": "synthetic",
+        "config": {"workload": f"{CONFIG_NAME}: 2-layer LSTM H1024 T128 B64/GPU fp32 forward (layers x timesteps DAG)",
+                   "batch_per_gpu": spec.batch, "global_batch": B_total, "algo": ex.algo,
+                   "parallelism": f"request-sharded x{world} (no collective)", "l2": "flushed (256 MiB write) before each timed step"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                     "kernel": f"recurrent wavefront ({ex.algo})", "kernel_ms_per_forward": rec_ms,
+                     "gemm_ms_per_forward": gemm_ms, "algorithmic_flops": rec_f,
+                     "peak_source": f"{peaks['source']} dense bf16 (burst)"},
+        "e2e": {"value": B_total * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "p50_ms": statistics.median(e2e_ms)},
+        "gpu_launches": ex.launches_per_forward() * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        info = cpu_info()
+        cb = time_cpu_baseline(spec, args.cpu_baseline_seconds, args.cpu_sample_batch)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": info["affinity"], "kind": "port",
+                                "sample": cb["sample"], "p50_ms": cb["p50_ms"], "host": info}
+        try:
+            line["cpu_baseline"]["torch_fused_fp32"] = torch_cpu_reference(spec, args.cpu_sample_batch)
+        except Exception as exc:  # context only
+            line["cpu_baseline"]["torch_fused_fp32"] = {"error": str(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/*
+ * hs_rnn.h — C ABI of the B200-native RNN DAG executor (libhsrnn.so).
+ *
+ * This is the seam under the reference's Python API.  The reference
+ * (`hetsched`) has no FFI: its executor is the virtual-time replay
+ * `engine.simulate` (/root/reference/pkg/src/hetsched/engine.py:265-418) and its
+ * profiler the seeded generator `synth_profile` (costmodel.py:176-221).  The
+ * entry points below replace those two seams with real B200 execution and
+ * timing; the Python wrapper (paper_2307_11339_b200/rnn.py) binds them with
+ * ctypes exactly as INTEGRATION.md shows.
+ *
+ *   reference seam                               replaced by
+ *   engine.simulate(graph, cm, plan) -> Trace    hs_rnn_forward / hs_rnn_forward_packed
+ *                                                (whole DAG, all-GPU plan segments)
+ *   engine.simulate, per-node NodeSpan           hs_rnn_run_cells (one layer-direction,
+ *                                                a contiguous run of timesteps = a GPU
+ *                                                segment of a hybrid plan)
+ *   costmodel.synth_profile -> W[:,0]            hs_rnn_profile (CUDA-event times per
+ *                                                layer-direction kernel)
+ *
+ * Conventions: every pointer argument that names a tensor is a DEVICE pointer
+ * allocated by the caller (PyTorch); the library never allocates or frees
+ * caller memory and keeps no state between calls apart from per-device
+ * attribute caches.  `stream` is a cudaStream_t passed as void*.  Returns
+ * HS_OK (0) or an HS_ERR_* code; hs_last_error() gives a thread-local message.
+ * No C++ exception crosses this boundary.  There is no CPU fallback: on a host
+ * without a usable sm_100 device every compute entry point fails.
+ *
+ * Tensor layouts (PyTorch nn.LSTM / nn.GRU, batch_first=False):
+ *   x      [T, B, I]             fp32
+ *   y      [T, B, dirs*H]        fp32
+ *   h0,hn  [layers*dirs, B, H]   fp32 (h0/c0 may be NULL = zeros)
+ *   c0,cn  [layers*dirs, B, H]   fp32 (LSTM only; NULL for GRU)
+ *   per layer-direction ld = l*dirs + d:
+ *     w_ih[ld] [G*H, I_l], w_hh[ld] [G*H, H], b_ih[ld] [G*H], b_hh[ld] [G*H]
+ *     I_0 = input, I_l = dirs*H for l >= 1; G = 4 (LSTM i,f,g,o) or 3 (GRU r,z,n)
+ */
+#ifndef HS_RNN_H
+#define HS_RNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_RNN_ABI_VERSION 1
+
+enum hs_cell { HS_CELL_LSTM = 0, HS_CELL_GRU = 1 };
+enum hs_dtype { HS_DTYPE_F32 = 0, HS_DTYPE_BF16 = 1 };
+enum hs_algo {
+  HS_ALGO_AUTO = 0,   /* pick the fastest path that supports the shape        */
+  HS_ALGO_SIMT = 1,   /* FP32 FFMA kernels (any shape; reference for the TC path) */
+  HS_ALGO_TC = 2      /* tcgen05 tensor-core kernels (split-bf16 in f32 mode)  */
+};
+enum hs_status {
+  HS_OK = 0,
+  HS_ERR_INVALID = 1,     /* bad descriptor / argument                      */
+  HS_ERR_CUDA = 2,        /* a CUDA runtime call failed                       */
+  HS_ERR_UNSUPPORTED = 3, /* shape/dtype/algo combination not implemented     */
+  HS_ERR_WORKSPACE = 4,   /* workspace or packed buffer too small             */
+  HS_ERR_NO_DEVICE = 5    /* no sm_100 device visible                         */
+};
+
+typedef struct hs_rnn_desc {
+  int32_t cell;    /* hs_cell */
+  int32_t layers;  /* L >= 1 */
+  int32_t dirs;    /* 1 or 2 */
+  int32_t input;   /* I (layer-0 input size) */
+  int32_t hidden;  /* H */
+  int32_t seq;     /* T */
+  int32_t batch;   /* B */
+  int32_t dtype;   /* hs_dtype: F32 = fp32-exact (max-abs 1e-4), BF16 = opt-in */
+  int32_t algo;    /* hs_algo */
+  int32_t reserved[7];
+} hs_rnn_desc;
+
+/* ABI version of the loaded library (HS_RNN_ABI_VERSION). */
+int hs_abi_version(void);
+
+/* Thread-local description of the last failure in this thread. */
+const char* hs_last_error(void);
+
+/* Which algorithm hs_rnn_forward_packed would run for this descriptor
+ * (HS_ALGO_SIMT or HS_ALGO_TC) on the current device. */
+int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo);
+
+/* Bytes of device workspace needed by hs_rnn_forward_packed / run_cells. */
+int hs_rnn_workspace(const hs_rnn_desc* desc, size_t* bytes);
+
+/* Bytes of the packed (kernel-layout) weight buffer. */
+int hs_rnn_packed_size(const hs_rnn_desc* desc, size_t* bytes);
+
+/* Repack PyTorch-layout weights (arrays of layers*dirs device pointers) into
+ * the kernel layout (bias folding, unit-block tiling, split-bf16 planes). */
+int hs_rnn_pack_weights(const hs_rnn_desc* desc,
+                        const void* const* w_ih, const void* const* w_hh,
+                        const void* const* b_ih, const void* const* b_hh,
+                        void* packed, size_t packed_bytes, void* stream);
+
+/* Whole-DAG forward with packed weights.  If `layer_ms` is non-NULL it must
+ * hold 2*layers floats: per layer, the input-projection GEMM time and the
+ * recurrent-wavefront time in ms (CUDA events; the call then synchronizes). */
+int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed,
+                          const void* x, const void* h0, const void* c0,
+                          void* y, void* hn, void* cn,
+                          void* workspace, size_t ws_bytes, void* stream,
+                          float* layer_ms);
+
+/* Convenience: pack + forward (weights in PyTorch layout).  Needs
+ * packed_size + workspace bytes of workspace. */
+int hs_rnn_forward(const hs_rnn_desc* desc, const void* x,
+                   const void* const* w_ih, const void* const* w_hh,
+                   const void* const* b_ih, const void* const* b_hh,
+                   const void* h0, const void* c0, void* y, void* hn, void* cn,
+                   void* workspace, size_t ws_bytes, void* stream);
+
+/* One GPU segment of a plan: timesteps t0..t1-1 (in the direction's own
+ * processing order) of layer-direction `ld`.  `in` is that layer's input
+ * [T, B, I_l], `out` its output [T, B, dirs*H] (columns d*H..d*H+H-1 are
+ * written), `h_prev`/`c_prev` [B, H] the state entering step t0 and
+ * `h_last`/`c_last` [B, H] receive the state after step t1-1.  `c_prev` and
+ * `c_last` are ignored for GRU. */
+int hs_rnn_run_cells(const hs_rnn_desc* desc, const void* packed, int32_t ld,
+                     int32_t t0, int32_t t1, const void* in, void* out,
+                     const void* h_prev, const void* c_prev,
+                     void* h_last, void* c_last,
+                     void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HS_RNN_H */

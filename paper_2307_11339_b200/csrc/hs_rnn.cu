@@ -1,0 +1,417 @@
+// libhsrnn.so — C ABI (include/hs_rnn.h) over the B200 RNN DAG kernels.
+//
+// Host-side responsibilities: descriptor validation, packed-weight and
+// workspace layout, algorithm selection (tcgen05 path vs SIMT path), launch
+// sequencing per layer (K1 input-projection GEMM, then the persistent
+// recurrent wavefront K2/K3), optional CUDA-event timing for the profiler.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hs_rnn.h"
+#include "simt_kernels.cuh"
+#include "tc_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define HS_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(HS_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Dims {
+  int G, L, D, I, H, T, B, dtype, algo_req;
+  int in_size(int l) const { return l == 0 ? I : D * H; }
+};
+
+int check_desc(const hs_rnn_desc* d, Dims* out) {
+  if (!d) return fail(HS_ERR_INVALID, "descriptor is NULL");
+  if (d->cell != HS_CELL_LSTM && d->cell != HS_CELL_GRU) return fail(HS_ERR_INVALID, "cell must be LSTM(0) or GRU(1), got %d", d->cell);
+  if (d->layers < 1) return fail(HS_ERR_INVALID, "layers must be >= 1, got %d", d->layers);
+  if (d->dirs != 1 && d->dirs != 2) return fail(HS_ERR_INVALID, "dirs must be 1 or 2, got %d", d->dirs);
+  if (d->input < 1 || d->hidden < 1 || d->seq < 1 || d->batch < 1)
+    return fail(HS_ERR_INVALID, "input/hidden/seq/batch must be positive (%d,%d,%d,%d)", d->input, d->hidden, d->seq, d->batch);
+  if (d->dtype != HS_DTYPE_F32 && d->dtype != HS_DTYPE_BF16) return fail(HS_ERR_INVALID, "dtype must be F32(0) or BF16(1), got %d", d->dtype);
+  if (d->algo < HS_ALGO_AUTO || d->algo > HS_ALGO_TC) return fail(HS_ERR_INVALID, "unknown algo %d", d->algo);
+  if (d->input % 4 || d->hidden % 4)
+    return fail(HS_ERR_UNSUPPORTED, "input and hidden sizes must be multiples of 4 (got %d, %d)", d->input, d->hidden);
+  Dims r;
+  r.G = d->cell == HS_CELL_LSTM ? 4 : 3;
+  r.L = d->layers; r.D = d->dirs; r.I = d->input; r.H = d->hidden; r.T = d->seq; r.B = d->batch;
+  r.dtype = d->dtype; r.algo_req = d->algo;
+  *out = r;
+  return HS_OK;
+}
+
+struct DeviceInfo {
+  int dev = -1, sms = 0, cc_major = 0, cc_minor = 0, occ_simt4 = 0, occ_simt3 = 0;
+  size_t smem_optin = 0;
+};
+
+int device_info(DeviceInfo* info) {
+  static thread_local DeviceInfo cache[16];
+  int dev;
+  HS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
+  DeviceInfo& c = cache[dev];
+  if (c.dev != dev) {
+    DeviceInfo n;
+    n.dev = dev;
+    HS_CUDA(cudaDeviceGetAttribute(&n.sms, cudaDevAttrMultiProcessorCount, dev));
+    HS_CUDA(cudaDeviceGetAttribute(&n.cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    HS_CUDA(cudaDeviceGetAttribute(&n.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    int optin = 0;
+    HS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    n.smem_optin = optin;
+    if (n.cc_major != 10) return fail(HS_ERR_NO_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a only", dev, n.cc_major, n.cc_minor);
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.occ_simt4, hs::recur_simt<4>, hs::RTHREADS, sizeof(hs::RecurSmem<4>)));
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.occ_simt3, hs::recur_simt<3>, hs::RTHREADS, sizeof(hs::RecurSmem<3>)));
+    c = n;
+  }
+  *info = c;
+  return HS_OK;
+}
+
+// ------------------------------------------------------------ packed layout
+struct LayerPack {
+  size_t wih, bias_x, bias_h, whh_simt;  // fp32 planes
+  size_t tc;                             // tensor-core planes (hs::tc layout), 0 if absent
+};
+struct PackLayout {
+  LayerPack ld[64];
+  size_t total;
+};
+
+int resolve_algo(const Dims& m, int* algo) {
+  const bool tc_ok = hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H);
+  if (m.algo_req == HS_ALGO_TC) {
+    if (!tc_ok) return fail(HS_ERR_UNSUPPORTED, "tensor-core path does not support H=%d B=%d", m.H, m.B);
+    *algo = HS_ALGO_TC;
+  } else if (m.algo_req == HS_ALGO_SIMT) {
+    if (m.dtype == HS_DTYPE_BF16) return fail(HS_ERR_UNSUPPORTED, "bf16 mode runs on the tensor-core path only");
+    *algo = HS_ALGO_SIMT;
+  } else {
+    *algo = (tc_ok && hs::tc::profitable(m.G, m.H, m.B, m.T)) || m.dtype == HS_DTYPE_BF16 ? HS_ALGO_TC : HS_ALGO_SIMT;
+    if (*algo == HS_ALGO_TC && !tc_ok) return fail(HS_ERR_UNSUPPORTED, "bf16 mode needs the tensor-core path, which does not support H=%d B=%d", m.H, m.B);
+  }
+  return HS_OK;
+}
+
+int pack_layout(const Dims& m, PackLayout* p) {
+  if (m.L * m.D > 64) return fail(HS_ERR_UNSUPPORTED, "at most 64 layer-directions");
+  size_t off = 0;
+  const int GH = m.G * m.H;
+  const int nub = (m.H + hs::RU - 1) / hs::RU;
+  for (int l = 0; l < m.L; ++l) {
+    for (int d = 0; d < m.D; ++d) {
+      LayerPack& lp = p->ld[l * m.D + d];
+      lp.wih = off;      off = align_up(off + sizeof(float) * (size_t)GH * m.in_size(l));
+      lp.bias_x = off;   off = align_up(off + sizeof(float) * GH);
+      lp.bias_h = off;   off = align_up(off + sizeof(float) * GH);
+      lp.whh_simt = off; off = align_up(off + sizeof(float) * (size_t)nub * m.H * m.G * hs::RU);
+      const size_t tcb = hs::tc::packed_bytes(m.G, m.H, m.in_size(l));
+      lp.tc = tcb ? off : 0;
+      off = align_up(off + tcb);
+    }
+  }
+  p->total = off;
+  return HS_OK;
+}
+
+// ----------------------------------------------------------------- workspace
+struct WsLayout {
+  size_t xproj, act0, act1, cst, zeros, barrier, tc, total;
+};
+
+WsLayout ws_layout(const Dims& m) {
+  WsLayout w{};
+  size_t off = 0;
+  const size_t TB = (size_t)m.T * m.B;
+  w.xproj = off;   off = align_up(off + sizeof(float) * m.D * TB * m.G * m.H);
+  w.act0 = off;    off = align_up(off + (m.L > 1 ? sizeof(float) * TB * m.D * m.H : 0));
+  w.act1 = off;    off = align_up(off + (m.L > 2 ? sizeof(float) * TB * m.D * m.H : 0));
+  w.cst = off;     off = align_up(off + sizeof(float) * m.D * m.B * m.H);
+  w.zeros = off;   off = align_up(off + sizeof(float) * m.D * m.B * m.H);
+  w.barrier = off; off = align_up(off + 256);
+  w.tc = off;      off = align_up(off + hs::tc::workspace_bytes(m.G, m.H, m.B, m.T, m.D, m.in_size(0)));
+  w.total = off;
+  return w;
+}
+
+template <typename T>
+T* at(void* base, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(base) + off); }
+template <typename T>
+const T* at(const void* base, size_t off) { return reinterpret_cast<const T*>(static_cast<const char*>(base) + off); }
+
+__global__ void bias_fold(const float* bi, const float* bh, float* bx, float* bhh, int GH, int lstm) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < GH; i += gridDim.x * blockDim.x) {
+    const float a = bi ? bi[i] : 0.f, b = bh ? bh[i] : 0.f;
+    bx[i] = lstm ? a + b : a;
+    bhh[i] = lstm ? 0.f : b;
+  }
+}
+
+int launch_gemm_simt(const float* A, const float* Bw, const float* bias, float* C, int M, int N, int K, cudaStream_t s) {
+  dim3 grid((N + 127) / 128, (M + 127) / 128);
+  hs::sgemm_tn_bias<<<grid, 256, 0, s>>>(A, Bw, bias, C, M, N, K);
+  HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+int launch_recur_simt(const Dims& m, const DeviceInfo& di, hs::RecurArgs& ra, cudaStream_t s) {
+  ra.tiles_u = (m.H + hs::RU - 1) / hs::RU;
+  ra.tiles_b = (m.B + hs::RB - 1) / hs::RB;
+  const int ntiles = ra.ndir * ra.tiles_u * ra.tiles_b;
+  const int occ = m.G == 4 ? di.occ_simt4 : di.occ_simt3;
+  if (occ < 1) return fail(HS_ERR_CUDA, "recurrent kernel cannot be resident");
+  int grid = di.sms * occ;
+  if (grid > ntiles) grid = ntiles;
+  HS_CUDA(cudaMemsetAsync(ra.barrier, 0, sizeof(unsigned int), s));
+  void* args[] = {&ra};
+  if (m.G == 4) {
+    HS_CUDA(cudaLaunchCooperativeKernel((const void*)hs::recur_simt<4>, dim3(grid), dim3(hs::RTHREADS), args, sizeof(hs::RecurSmem<4>), s));
+  } else {
+    HS_CUDA(cudaLaunchCooperativeKernel((const void*)hs::recur_simt<3>, dim3(grid), dim3(hs::RTHREADS), args, sizeof(hs::RecurSmem<3>), s));
+  }
+  return HS_OK;
+}
+
+int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout& pl, const void* packed,
+                 const float* x, const float* h0, const float* c0, float* y, float* hn, float* cn,
+                 void* ws, const WsLayout& wl, cudaStream_t s, float* layer_ms) {
+  const size_t DBH = (size_t)m.D * m.B * m.H;
+  float* zeros = at<float>(ws, wl.zeros);
+  if (!h0 || (m.G == 4 && !c0)) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
+  cudaEvent_t evs[2 * 64 + 1];
+  const int nev = layer_ms ? 2 * m.L + 1 : 0;
+  for (int i = 0; i < nev; ++i) HS_CUDA(cudaEventCreate(&evs[i]));
+  if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
+  const size_t TB = (size_t)m.T * m.B;
+  const float* in = x;
+  for (int l = 0; l < m.L; ++l) {
+    float* out = (l == m.L - 1) ? y : at<float>(ws, (l & 1) ? wl.act1 : wl.act0);
+    const int Il = m.in_size(l);
+    hs::RecurArgs ra{};
+    ra.H = m.H; ra.B = m.B; ra.T = m.T; ra.D = m.D;
+    ra.dir_lo = 0; ra.ndir = m.D; ra.s0 = 0; ra.s1 = m.T;
+    ra.out = out;
+    ra.cst = at<float>(ws, wl.cst);
+    ra.barrier = at<unsigned int>(ws, wl.barrier);
+    for (int d = 0; d < m.D; ++d) {
+      const int ld = l * m.D + d;
+      const LayerPack& lp = pl.ld[ld];
+      float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
+      if (algo == HS_ALGO_TC) {
+        int rc = hs::tc::input_projection(m.G, m.H, Il, (int)TB, in, at<unsigned char>(packed, lp.tc),
+                                          at<float>(packed, lp.bias_x), xp, at<unsigned char>(ws, wl.tc), m.dtype, s, g_err);
+        if (rc) return rc;
+      } else {
+        int rc = launch_gemm_simt(in, at<float>(packed, lp.wih), at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, s);
+        if (rc) return rc;
+      }
+      ra.whh[d] = at<float>(packed, lp.whh_simt);
+      ra.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+      ra.xproj[d] = xp;
+      ra.hprev[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+      ra.cprev[d] = c0 ? c0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+      ra.hlast[d] = hn + (size_t)ld * m.B * m.H;
+      ra.clast[d] = cn ? cn + (size_t)ld * m.B * m.H : ra.cst + (size_t)d * m.B * m.H;
+    }
+    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
+    if (algo == HS_ALGO_TC) {
+      int rc = hs::tc::recurrence(m.G, m.H, m.B, m.T, m.D, ra, packed, pl.ld + l * m.D, at<unsigned char>(ws, wl.tc), m.dtype, di.sms, s, g_err);
+      if (rc) return rc;
+    } else {
+      int rc = launch_recur_simt(m, di, ra, s);
+      if (rc) return rc;
+    }
+    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
+    in = out;
+  }
+  if (nev) {
+    HS_CUDA(cudaEventSynchronize(evs[nev - 1]));
+    for (int l = 0; l < m.L; ++l) {
+      HS_CUDA(cudaEventElapsedTime(&layer_ms[2 * l], evs[2 * l], evs[2 * l + 1]));
+      HS_CUDA(cudaEventElapsedTime(&layer_ms[2 * l + 1], evs[2 * l + 1], evs[2 * l + 2]));
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  }
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hs_abi_version(void) { return HS_RNN_ABI_VERSION; }
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+
+int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!algo) return fail(HS_ERR_INVALID, "algo out-pointer is NULL");
+  int a;
+  rc = resolve_algo(m, &a);
+  if (rc) return rc;
+  *algo = a;
+  return HS_OK;
+}
+
+int hs_rnn_workspace(const hs_rnn_desc* desc, size_t* bytes) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!bytes) return fail(HS_ERR_INVALID, "bytes out-pointer is NULL");
+  *bytes = ws_layout(m).total;
+  return HS_OK;
+}
+
+int hs_rnn_packed_size(const hs_rnn_desc* desc, size_t* bytes) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!bytes) return fail(HS_ERR_INVALID, "bytes out-pointer is NULL");
+  PackLayout pl;
+  rc = pack_layout(m, &pl);
+  if (rc) return rc;
+  *bytes = pl.total;
+  return HS_OK;
+}
+
+int hs_rnn_pack_weights(const hs_rnn_desc* desc, const void* const* w_ih, const void* const* w_hh,
+                        const void* const* b_ih, const void* const* b_hh, void* packed, size_t packed_bytes,
+                        void* stream) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!w_ih || !w_hh || !packed) return fail(HS_ERR_INVALID, "w_ih, w_hh and packed must be non-NULL");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  if (packed_bytes < pl.total) return fail(HS_ERR_WORKSPACE, "packed buffer has %zu bytes, needs %zu", packed_bytes, pl.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int GH = m.G * m.H;
+  for (int l = 0; l < m.L; ++l) {
+    for (int d = 0; d < m.D; ++d) {
+      const int ld = l * m.D + d;
+      if (!w_ih[ld] || !w_hh[ld]) return fail(HS_ERR_INVALID, "weights of layer-direction %d are NULL", ld);
+      const LayerPack& lp = pl.ld[ld];
+      HS_CUDA(cudaMemcpyAsync(at<float>(packed, lp.wih), w_ih[ld], sizeof(float) * (size_t)GH * m.in_size(l), cudaMemcpyDeviceToDevice, s));
+      bias_fold<<<(GH + 255) / 256, 256, 0, s>>>(b_ih ? static_cast<const float*>(b_ih[ld]) : nullptr,
+                                                 b_hh ? static_cast<const float*>(b_hh[ld]) : nullptr,
+                                                 at<float>(packed, lp.bias_x), at<float>(packed, lp.bias_h), GH, m.G == 4);
+      HS_CUDA(cudaGetLastError());
+      hs::pack_whh_simt<<<4 * di.sms, 256, 0, s>>>(static_cast<const float*>(w_hh[ld]), at<float>(packed, lp.whh_simt), m.G, m.H);
+      HS_CUDA(cudaGetLastError());
+      if (lp.tc) {
+        rc = hs::tc::pack_layer(m.G, m.H, m.in_size(l), static_cast<const float*>(w_ih[ld]), static_cast<const float*>(w_hh[ld]),
+                                at<unsigned char>(packed, lp.tc), s, g_err);
+        if (rc) return rc;
+      }
+    }
+  }
+  return HS_OK;
+}
+
+int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed, const void* x, const void* h0, const void* c0,
+                          void* y, void* hn, void* cn, void* workspace, size_t ws_bytes, void* stream, float* layer_ms) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!packed || !x || !y || !hn || !workspace) return fail(HS_ERR_INVALID, "packed, x, y, hn and workspace must be non-NULL");
+  if (m.G == 4 && !cn) return fail(HS_ERR_INVALID, "LSTM needs a c_n output");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  WsLayout wl = ws_layout(m);
+  if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
+  return forward_impl(m, algo, di, pl, packed, static_cast<const float*>(x), static_cast<const float*>(h0),
+                      static_cast<const float*>(c0), static_cast<float*>(y), static_cast<float*>(hn),
+                      static_cast<float*>(cn), workspace, wl, static_cast<cudaStream_t>(stream), layer_ms);
+}
+
+int hs_rnn_forward(const hs_rnn_desc* desc, const void* x, const void* const* w_ih, const void* const* w_hh,
+                   const void* const* b_ih, const void* const* b_hh, const void* h0, const void* c0, void* y,
+                   void* hn, void* cn, void* workspace, size_t ws_bytes, void* stream) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  const size_t need = align_up(pl.total) + ws_layout(m).total;
+  if (!workspace || ws_bytes < need) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu (packed + scratch)", ws_bytes, need);
+  void* packed = workspace;
+  void* scratch = static_cast<char*>(workspace) + align_up(pl.total);
+  if ((rc = hs_rnn_pack_weights(desc, w_ih, w_hh, b_ih, b_hh, packed, pl.total, stream))) return rc;
+  return hs_rnn_forward_packed(desc, packed, x, h0, c0, y, hn, cn, scratch, ws_bytes - align_up(pl.total), stream, nullptr);
+}
+
+int hs_rnn_run_cells(const hs_rnn_desc* desc, const void* packed, int32_t ld, int32_t t0, int32_t t1, const void* in,
+                     void* out, const void* h_prev, const void* c_prev, void* h_last, void* c_last, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (ld < 0 || ld >= m.L * m.D) return fail(HS_ERR_INVALID, "layer-direction %d out of range", ld);
+  if (t0 < 0 || t1 > m.T || t0 >= t1) return fail(HS_ERR_INVALID, "step range [%d, %d) invalid for T=%d", t0, t1, m.T);
+  if (!packed || !in || !out || !h_prev || !h_last || !workspace) return fail(HS_ERR_INVALID, "NULL tensor argument");
+  if (m.G == 4 && (!c_prev || !c_last)) return fail(HS_ERR_INVALID, "LSTM needs c_prev and c_last");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  WsLayout wl = ws_layout(m);
+  if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int l = ld / m.D, d = ld % m.D;
+  const LayerPack& lp = pl.ld[ld];
+  // Input projection for the processed timesteps only: rows [tlo, thi) of `in`.
+  const int tlo = d == 0 ? t0 : m.T - t1, thi = d == 0 ? t1 : m.T - t0;
+  float* xp = at<float>(workspace, wl.xproj) + (size_t)d * m.T * m.B * m.G * m.H;
+  const size_t row0 = (size_t)tlo * m.B;
+  rc = launch_gemm_simt(static_cast<const float*>(in) + row0 * m.in_size(l), at<float>(packed, lp.wih),
+                        at<float>(packed, lp.bias_x), xp + row0 * m.G * m.H, (thi - tlo) * m.B, m.G * m.H, m.in_size(l), s);
+  if (rc) return rc;
+  hs::RecurArgs ra{};
+  ra.H = m.H; ra.B = m.B; ra.T = m.T; ra.D = m.D;
+  ra.dir_lo = d; ra.ndir = 1; ra.s0 = t0; ra.s1 = t1;
+  ra.out = static_cast<float*>(out);
+  ra.cst = at<float>(workspace, wl.cst);
+  ra.barrier = at<unsigned int>(workspace, wl.barrier);
+  ra.whh[d] = at<float>(packed, lp.whh_simt);
+  ra.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+  ra.xproj[d] = xp;
+  ra.hprev[d] = static_cast<const float*>(h_prev);
+  ra.cprev[d] = static_cast<const float*>(c_prev);
+  ra.hlast[d] = static_cast<float*>(h_last);
+  ra.clast[d] = m.G == 4 ? static_cast<float*>(c_last) : ra.cst;
+  return launch_recur_simt(m, di, ra, s);
+}
+
+}  // extern "C"

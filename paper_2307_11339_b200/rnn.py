@@ -1,0 +1,322 @@
+"""RNN model spec, synthetic weights, and the ctypes binding of libhsrnn.so.
+
+This is the host side of the drop-in boundary (include/hs_rnn.h).  PyTorch
+provides device memory and streams; every byte of compute runs in the
+library's sm_100a kernels.  There is no CPU fallback: if the library is
+missing or no sm_100 device is visible, :func:`load_library` and
+:class:`RNNExecutor` raise.
+
+Synthetic data follows SURVEY §8(d): weights ~ U(-1/sqrt(H), 1/sqrt(H)) (the
+``nn.LSTM/GRU.reset_parameters`` default) drawn on CPU from
+``torch.Generator().manual_seed(seed)``; inputs ~ U(-1, 1) with seed 1.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, replace
+from pathlib import Path
+
+import torch
+
+from . import build as _build
+
+__all__ = [
+    "RNNSpec",
+    "CONFIGS",
+    "HsRnnError",
+    "load_library",
+    "init_weights",
+    "make_input",
+    "RNNExecutor",
+    "ABI_SYMBOLS",
+]
+
+CELLS = {"lstm": 0, "gru": 1}
+DTYPES = {"f32": 0, "bf16": 1}
+ALGOS = {"auto": 0, "simt": 1, "tc": 2}
+ALGO_NAMES = {1: "simt", 2: "tc"}
+GATES = {"lstm": 4, "gru": 3}
+
+#: every symbol declared in include/hs_rnn.h
+ABI_SYMBOLS = (
+    "hs_abi_version",
+    "hs_last_error",
+    "hs_rnn_resolve_algo",
+    "hs_rnn_workspace",
+    "hs_rnn_packed_size",
+    "hs_rnn_pack_weights",
+    "hs_rnn_forward_packed",
+    "hs_rnn_forward",
+    "hs_rnn_run_cells",
+)
+
+
+class HsRnnError(RuntimeError):
+    """A libhsrnn.so call returned a non-zero status."""
+
+    def __init__(self, func: str, code: int, msg: str):
+        super().__init__(f"{func} failed (status {code}): {msg}")
+        self.code = code
+
+
+@dataclass(frozen=True)
+class RNNSpec:
+    """Shape of a stacked (bi)directional LSTM/GRU; ``input`` defaults to H."""
+
+    cell: str
+    layers: int
+    hidden: int
+    seq: int
+    batch: int
+    input: int | None = None
+    dirs: int = 1
+    dtype: str = "f32"
+    algo: str = "auto"
+
+    def __post_init__(self):
+        if self.cell not in CELLS:
+            raise ValueError(f"cell must be one of {sorted(CELLS)}, got {self.cell!r}")
+        if self.dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {self.dtype!r}")
+        if self.algo not in ALGOS:
+            raise ValueError(f"algo must be one of {sorted(ALGOS)}, got {self.algo!r}")
+        if self.dirs not in (1, 2):
+            raise ValueError(f"dirs must be 1 or 2, got {self.dirs}")
+        for name in ("layers", "hidden", "seq", "batch"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be positive")
+
+    @property
+    def I(self) -> int:
+        return self.hidden if self.input is None else self.input
+
+    @property
+    def G(self) -> int:
+        return GATES[self.cell]
+
+    def layer_input(self, l: int) -> int:
+        return self.I if l == 0 else self.dirs * self.hidden
+
+    def with_(self, **kw) -> "RNNSpec":
+        return replace(self, **kw)
+
+    def flops(self) -> tuple[float, float]:
+        """(input-projection, recurrent) FLOPs of one forward."""
+        G, H, T, B = self.G, self.hidden, self.seq, self.batch
+        gemm = sum(2.0 * T * B * G * H * self.layer_input(l) for l in range(self.layers)) * self.dirs
+        rec = 2.0 * T * B * G * H * H * self.layers * self.dirs
+        return gemm, rec
+
+
+#: BASELINE.json configs c1..c5
+CONFIGS: dict[str, RNNSpec] = {
+    "c1": RNNSpec("lstm", 1, 128, 16, 1),
+    "c2": RNNSpec("lstm", 2, 1024, 128, 64),
+    "c3": RNNSpec("gru", 4, 512, 256, 32),
+    "c4": RNNSpec("lstm", 8, 2048, 512, 16),
+    "c5": RNNSpec("lstm", 3, 1024, 1024, 256, dirs=2, dtype="bf16"),
+}
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [
+        ("cell", ctypes.c_int32),
+        ("layers", ctypes.c_int32),
+        ("dirs", ctypes.c_int32),
+        ("input", ctypes.c_int32),
+        ("hidden", ctypes.c_int32),
+        ("seq", ctypes.c_int32),
+        ("batch", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("algo", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+def make_desc(spec: RNNSpec) -> _Desc:
+    return _Desc(
+        CELLS[spec.cell], spec.layers, spec.dirs, spec.I, spec.hidden, spec.seq, spec.batch,
+        DTYPES[spec.dtype], ALGOS[spec.algo],
+    )
+
+
+_LIB: ctypes.CDLL | None = None
+
+
+def load_library(path: str | Path | None = None, build_if_missing: bool = False) -> ctypes.CDLL:
+    """Load libhsrnn.so (in-tree).  Raises if it is absent — there is no
+    fallback implementation."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    lib_path = Path(path) if path else _build.library_path()
+    if not lib_path.exists():
+        if build_if_missing:
+            lib_path = _build.build()
+        else:
+            raise RuntimeError(
+                f"{lib_path} is missing: build it with `python -m paper_2307_11339_b200.build` "
+                "(there is no CPU fallback for the RNN executor)"
+            )
+    lib = ctypes.CDLL(str(lib_path))
+    vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32
+    pd = ctypes.POINTER(_Desc)
+    pvp = ctypes.POINTER(vp)
+    lib.hs_abi_version.restype = ctypes.c_int
+    lib.hs_last_error.restype = ctypes.c_char_p
+    lib.hs_rnn_resolve_algo.argtypes = [pd, ctypes.POINTER(i32)]
+    lib.hs_rnn_workspace.argtypes = [pd, ctypes.POINTER(sz)]
+    lib.hs_rnn_packed_size.argtypes = [pd, ctypes.POINTER(sz)]
+    lib.hs_rnn_pack_weights.argtypes = [pd, pvp, pvp, pvp, pvp, vp, sz, vp]
+    lib.hs_rnn_forward_packed.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, ctypes.POINTER(ctypes.c_float)]
+    lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    for name in ABI_SYMBOLS[2:]:
+        getattr(lib, name).restype = ctypes.c_int
+    if lib.hs_abi_version() != 1:
+        raise RuntimeError(f"{lib_path}: ABI version {lib.hs_abi_version()} != 1")
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def _check(lib, func: str, code: int) -> None:
+    if code != 0:
+        raise HsRnnError(func, code, lib.hs_last_error().decode(errors="replace"))
+
+
+def init_weights(spec: RNNSpec, seed: int = 0) -> list[dict[str, torch.Tensor]]:
+    """PyTorch-default init U(-1/sqrt(H), 1/sqrt(H)); CPU fp32 tensors, one dict
+    per layer-direction ``l*dirs + d``, drawn in (w_ih, w_hh, b_ih, b_hh) order."""
+    gen = torch.Generator().manual_seed(seed)
+    bound = 1.0 / math.sqrt(spec.hidden)
+    GH = spec.G * spec.hidden
+    out = []
+    for l in range(spec.layers):
+        for _d in range(spec.dirs):
+            shapes = {
+                "w_ih": (GH, spec.layer_input(l)),
+                "w_hh": (GH, spec.hidden),
+                "b_ih": (GH,),
+                "b_hh": (GH,),
+            }
+            out.append({k: (torch.rand(s, generator=gen) * 2.0 - 1.0) * bound for k, s in shapes.items()})
+    return out
+
+
+def make_input(spec: RNNSpec, seed: int = 1, batch: int | None = None) -> torch.Tensor:
+    """x ~ U(-1, 1), shape [T, B, I], CPU fp32."""
+    gen = torch.Generator().manual_seed(seed)
+    B = spec.batch if batch is None else batch
+    return torch.rand((spec.seq, B, spec.I), generator=gen) * 2.0 - 1.0
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+class RNNExecutor:
+    """A (bi)directional LSTM/GRU resident on one B200.
+
+    Construction copies the weights to the device and repacks them into the
+    kernel layout once (``hs_rnn_pack_weights``); :meth:`forward` then runs
+    the whole layers x timesteps DAG with the packed weights.
+    """
+
+    def __init__(self, spec: RNNSpec, weights, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("RNNExecutor needs a CUDA (sm_100) device; there is no CPU fallback")
+        self.spec = spec
+        self.lib = load_library()
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self.desc = make_desc(spec)
+        with torch.cuda.device(self.device):
+            a = ctypes.c_int32()
+            _check(self.lib, "hs_rnn_resolve_algo", self.lib.hs_rnn_resolve_algo(ctypes.byref(self.desc), ctypes.byref(a)))
+            self.algo = ALGO_NAMES[a.value]
+            n = ctypes.c_size_t()
+            _check(self.lib, "hs_rnn_packed_size", self.lib.hs_rnn_packed_size(ctypes.byref(self.desc), ctypes.byref(n)))
+            self.packed = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
+            _check(self.lib, "hs_rnn_workspace", self.lib.hs_rnn_workspace(ctypes.byref(self.desc), ctypes.byref(n)))
+            self.workspace = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
+            self.weights = [
+                {k: v.to(self.device, torch.float32).contiguous() for k, v in w.items()} for w in weights
+            ]
+            if len(self.weights) != spec.layers * spec.dirs:
+                raise ValueError(f"expected {spec.layers * spec.dirs} layer-direction weight sets, got {len(weights)}")
+            for ld, w in enumerate(self.weights):
+                l = ld // spec.dirs
+                GH = spec.G * spec.hidden
+                want = {"w_ih": (GH, spec.layer_input(l)), "w_hh": (GH, spec.hidden), "b_ih": (GH,), "b_hh": (GH,)}
+                for k, shp in want.items():
+                    if tuple(w[k].shape) != shp:
+                        raise ValueError(f"layer-direction {ld}: {k} has shape {tuple(w[k].shape)}, expected {shp}")
+            stream = torch.cuda.current_stream(self.device)
+            arrs = [_ptr_array([w[k] for w in self.weights]) for k in ("w_ih", "w_hh", "b_ih", "b_hh")]
+            _check(
+                self.lib,
+                "hs_rnn_pack_weights",
+                self.lib.hs_rnn_pack_weights(
+                    ctypes.byref(self.desc), *arrs, self.packed.data_ptr(), self.packed.numel(), stream.cuda_stream
+                ),
+            )
+
+    def launches_per_forward(self) -> int:
+        """Kernels this library launches per forward (memsets excluded):
+        per layer one input-projection GEMM per direction plus one persistent
+        recurrent kernel covering both directions."""
+        s = self.spec
+        return s.layers * (s.dirs + 1)
+
+    def alloc_outputs(self, batch: int | None = None):
+        s = self.spec
+        B = s.batch if batch is None else batch
+        y = torch.empty((s.seq, B, s.dirs * s.hidden), device=self.device)
+        hn = torch.empty((s.layers * s.dirs, B, s.hidden), device=self.device)
+        cn = torch.empty_like(hn) if s.cell == "lstm" else None
+        return y, hn, cn
+
+    def forward(self, x: torch.Tensor, h0=None, c0=None, out=None, layer_ms: bool = False):
+        """Run the DAG on device tensors.  Returns ``(y, h_n, c_n)`` (c_n None
+        for GRU), plus per-layer [gemm_ms, recurrent_ms] when ``layer_ms``."""
+        s = self.spec
+        if x.device != self.device or x.dtype != torch.float32 or not x.is_contiguous():
+            raise ValueError("x must be a contiguous float32 tensor on the executor's device")
+        if tuple(x.shape) != (s.seq, s.batch, s.I):
+            raise ValueError(f"x has shape {tuple(x.shape)}, expected {(s.seq, s.batch, s.I)}")
+        y, hn, cn = out if out is not None else self.alloc_outputs()
+        times = (ctypes.c_float * (2 * s.layers))() if layer_ms else None
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            _check(
+                self.lib,
+                "hs_rnn_forward_packed",
+                self.lib.hs_rnn_forward_packed(
+                    ctypes.byref(self.desc), self.packed.data_ptr(), x.data_ptr(), ptr(h0), ptr(c0),
+                    y.data_ptr(), hn.data_ptr(), ptr(cn), self.workspace.data_ptr(), self.workspace.numel(),
+                    stream.cuda_stream, times,
+                ),
+            )
+        if layer_ms:
+            return y, hn, cn, [[times[2 * l], times[2 * l + 1]] for l in range(s.layers)]
+        return y, hn, cn
+
+    def run_cells(self, ld: int, t0: int, t1: int, inp, out, h_prev, c_prev, h_last, c_last):
+        """Steps ``t0..t1-1`` (processing order) of layer-direction ``ld``."""
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            _check(
+                self.lib,
+                "hs_rnn_run_cells",
+                self.lib.hs_rnn_run_cells(
+                    ctypes.byref(self.desc), self.packed.data_ptr(), ld, t0, t1, ptr(inp), ptr(out),
+                    ptr(h_prev), ptr(c_prev), ptr(h_last), ptr(c_last), self.workspace.data_ptr(),
+                    self.workspace.numel(), stream.cuda_stream,
+                ),
+            )

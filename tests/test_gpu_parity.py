@@ -1,0 +1,130 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the float64
+oracle.  Tolerance: max-abs <= 1e-4 in f32 mode (BASELINE.json north_star);
+bf16 opt-in mode: max-abs <= 1e-2."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.rnn_ref import rnn_forward_ref
+from paper_2307_11339_b200 import CONFIGS, RNNExecutor, RNNSpec, init_weights, make_input
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-4
+TOL_BF16 = 1e-2
+
+
+def np_w(weights):
+    return [{k: v.double().numpy() for k, v in w.items()} for w in weights]
+
+
+def run_both(spec, seed=0, h0=None, c0=None):
+    w = init_weights(spec, seed)
+    x = make_input(spec, seed + 1)
+    ex = RNNExecutor(spec, w)
+    dev = ex.device
+    y, hn, cn = ex.forward(x.to(dev), None if h0 is None else h0.to(dev), None if c0 is None else c0.to(dev))
+    torch.cuda.synchronize()
+    ref = rnn_forward_ref(spec.cell, x.double().numpy(), np_w(w),
+                          None if h0 is None else h0.double().numpy(),
+                          None if c0 is None else c0.double().numpy(), dirs=spec.dirs)
+    got = (y.cpu().double().numpy(), hn.cpu().double().numpy(), None if cn is None else cn.cpu().double().numpy())
+    return ex, got, ref
+
+
+def max_err(got, ref):
+    return max(float(np.abs(g - r).max()) for g, r in zip(got, ref) if r is not None)
+
+
+SMALL = [
+    CONFIGS["c1"],
+    RNNSpec("lstm", 2, 36, 7, 3, input=20),
+    RNNSpec("gru", 3, 44, 9, 5, input=12),
+    RNNSpec("lstm", 2, 20, 6, 33, dirs=2),
+    RNNSpec("gru", 2, 16, 5, 2, input=8, dirs=2),
+    RNNSpec("lstm", 1, 128, 3, 70),
+]
+
+
+@pytest.mark.parametrize("spec", SMALL, ids=lambda s: f"{s.cell}{s.layers}x{s.hidden}T{s.seq}B{s.batch}d{s.dirs}")
+@pytest.mark.parametrize("algo", ["simt", "auto"])
+def test_small_shapes(spec, algo):
+    _ex, got, ref = run_both(spec.with_(algo=algo))
+    assert max_err(got, ref) <= TOL_F32
+
+
+def test_c1_matches_golden_fixture(golden_dir):
+    gold = np.load(golden_dir / "tensor_c1.npz")
+    spec = CONFIGS["c1"]
+    ex = RNNExecutor(spec, init_weights(spec, 0))
+    x = torch.from_numpy(gold["x"]).to(ex.device)
+    y, hn, cn = ex.forward(x)
+    assert float((y.cpu().double() - torch.from_numpy(gold["y"])).abs().max()) <= TOL_F32
+    assert float((hn.cpu().double() - torch.from_numpy(gold["hn"])).abs().max()) <= TOL_F32
+    assert float((cn.cpu().double() - torch.from_numpy(gold["cn"])).abs().max()) <= TOL_F32
+
+
+def test_initial_states():
+    spec = RNNSpec("lstm", 2, 64, 10, 4)
+    g = torch.Generator().manual_seed(5)
+    h0 = torch.rand((2, 4, 64), generator=g) - 0.5
+    c0 = torch.rand((2, 4, 64), generator=g) - 0.5
+    _ex, got, ref = run_both(spec, h0=h0, c0=c0)
+    assert max_err(got, ref) <= TOL_F32
+
+
+@pytest.mark.parametrize("algo", ["simt", "auto"])
+def test_c2_full_size(algo):
+    """BASELINE target config: 2-layer LSTM H1024 T128 B64, f32, max-abs 1e-4."""
+    _ex, got, ref = run_both(CONFIGS["c2"].with_(algo=algo))
+    err = max_err(got, ref)
+    print(f"c2 {algo} max-abs {err:.3e}")
+    assert err <= TOL_F32
+
+
+def test_c3_full_size():
+    _ex, got, ref = run_both(CONFIGS["c3"])
+    err = max_err(got, ref)
+    print(f"c3 max-abs {err:.3e}")
+    assert err <= TOL_F32
+
+
+def test_c4_reduced_seq():
+    """c4 at full width/depth (8 x 2048, B16) on T=24 (the oracle is float64 numpy)."""
+    _ex, got, ref = run_both(CONFIGS["c4"].with_(seq=24))
+    assert max_err(got, ref) <= TOL_F32
+
+
+def test_deterministic_repeat():
+    spec = CONFIGS["c2"].with_(seq=16)
+    w = init_weights(spec)
+    ex = RNNExecutor(spec, w)
+    x = make_input(spec).to(ex.device)
+    a = [t.clone() for t in ex.forward(x)]
+    b = ex.forward(x)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+
+
+def test_run_cells_segments_equal_whole():
+    """A plan's GPU segments (hs_rnn_run_cells) chained over every layer and a
+    split point reproduce the fused forward bit-for-bit."""
+    spec = RNNSpec("lstm", 2, 48, 12, 3)
+    w = init_weights(spec, 2)
+    ex = RNNExecutor(spec, w)
+    dev = ex.device
+    x = make_input(spec, 3).to(dev)
+    y, hn, cn = ex.forward(x)
+    H, B, T = spec.hidden, spec.batch, spec.seq
+    inp = x
+    for l in range(spec.layers):
+        out = torch.zeros((T, B, H), device=dev)
+        h = torch.zeros((B, H), device=dev)
+        c = torch.zeros((B, H), device=dev)
+        for t0, t1 in ((0, 5), (5, 12)):
+            h2, c2 = torch.empty_like(h), torch.empty_like(c)
+            ex.run_cells(l, t0, t1, inp, out, h, c, h2, c2)
+            h, c = h2, c2
+        assert torch.equal(h, hn[l]) and torch.equal(c, cn[l])
+        inp = out
+    assert torch.equal(inp, y)
