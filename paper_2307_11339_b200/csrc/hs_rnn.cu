@@ -103,7 +103,7 @@ struct PackLayout {
 };
 
 int resolve_algo(const Dims& m, int* algo) {
-  const bool tc_ok = hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H);
+  const bool tc_ok = hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H, m.D, m.dtype == HS_DTYPE_BF16 ? 1 : 2);
   if (m.algo_req == HS_ALGO_TC) {
     if (!tc_ok) return fail(HS_ERR_UNSUPPORTED, "tensor-core path does not support H=%d B=%d", m.H, m.B);
     *algo = HS_ALGO_TC;
@@ -196,9 +196,77 @@ int launch_recur_simt(const Dims& m, const DeviceInfo& di, hs::RecurArgs& ra, cu
   return HS_OK;
 }
 
+
+// Tensor-core forward: per layer, split the input into bf16 planes (layer 0;
+// later layers get their planes straight from the previous recurrence
+// epilogue), K1 GEMM per direction, then one recurrent launch (both dirs).
+int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const void* packed, const float* x,
+               const float* h0, const float* c0, float* y, float* hn, float* cn, void* ws, const WsLayout& wl,
+               cudaStream_t s, float* layer_ms) {
+  using namespace hs::tc;
+  const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
+  const size_t TB = (size_t)m.T * m.B;
+  const size_t DBH = (size_t)m.D * m.B * m.H;
+  float* zeros = at<float>(ws, wl.zeros);
+  if (!h0 || (m.G == 4 && !c0)) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
+  const TcWs tw = tc_ws_layout(m.G, m.H, m.B, m.T, m.D, m.I);
+  unsigned char* tcws = at<unsigned char>(ws, wl.tc);
+  __nv_bfloat16* xpl = reinterpret_cast<__nv_bfloat16*>(tcws + tw.xpl);
+  __nv_bfloat16* hbuf = reinterpret_cast<__nv_bfloat16*>(tcws + tw.hbuf);
+  unsigned int* counters = reinterpret_cast<unsigned int*>(tcws + tw.counters);
+  cudaEvent_t evs[2 * 64 + 1];
+  const int nev = layer_ms ? 2 * m.L + 1 : 0;
+  for (int i = 0; i < nev; ++i) HS_CUDA(cudaEventCreate(&evs[i]));
+  if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
+  int rc = split_planes(x, xpl, TB, m.I, s, g_err);
+  if (rc) return rc;
+  for (int l = 0; l < m.L; ++l) {
+    const int Il = m.in_size(l);
+    TcRecurArgs a{};
+    a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D;
+    const __nv_bfloat16* whh[2] = {nullptr, nullptr};
+    for (int d = 0; d < m.D; ++d) {
+      const int ld = l * m.D + d;
+      const LayerPack& lp = pl.ld[ld];
+      const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
+      whh[d] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
+      float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
+      rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
+      if (rc) return rc;
+      a.xproj[d] = xp;
+      a.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+      a.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+      a.c0[d] = c0 ? c0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+      a.hn[d] = hn + (size_t)ld * m.B * m.H;
+      a.cn[d] = cn ? cn + (size_t)ld * m.B * m.H : nullptr;
+    }
+    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
+    const bool last = l == m.L - 1;
+    a.y = last ? y : nullptr;
+    a.ypl = last ? nullptr : xpl;
+    a.hbuf = hbuf;
+    a.counters = counters;
+    HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
+    HS_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
+    if (rc) return rc;
+    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
+  }
+  if (nev) {
+    HS_CUDA(cudaEventSynchronize(evs[nev - 1]));
+    for (int l = 0; l < m.L; ++l) {
+      HS_CUDA(cudaEventElapsedTime(&layer_ms[2 * l], evs[2 * l], evs[2 * l + 1]));
+      HS_CUDA(cudaEventElapsedTime(&layer_ms[2 * l + 1], evs[2 * l + 1], evs[2 * l + 2]));
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  }
+  return HS_OK;
+}
+
 int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout& pl, const void* packed,
                  const float* x, const float* h0, const float* c0, float* y, float* hn, float* cn,
                  void* ws, const WsLayout& wl, cudaStream_t s, float* layer_ms) {
+  if (algo == HS_ALGO_TC) return tc_forward(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, layer_ms);
   const size_t DBH = (size_t)m.D * m.B * m.H;
   float* zeros = at<float>(ws, wl.zeros);
   if (!h0 || (m.G == 4 && !c0)) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
@@ -221,14 +289,8 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
       const int ld = l * m.D + d;
       const LayerPack& lp = pl.ld[ld];
       float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
-      if (algo == HS_ALGO_TC) {
-        int rc = hs::tc::input_projection(m.G, m.H, Il, (int)TB, in, at<unsigned char>(packed, lp.tc),
-                                          at<float>(packed, lp.bias_x), xp, at<unsigned char>(ws, wl.tc), m.dtype, s, g_err);
-        if (rc) return rc;
-      } else {
-        int rc = launch_gemm_simt(in, at<float>(packed, lp.wih), at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, s);
-        if (rc) return rc;
-      }
+      int rc = launch_gemm_simt(in, at<float>(packed, lp.wih), at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, s);
+      if (rc) return rc;
       ra.whh[d] = at<float>(packed, lp.whh_simt);
       ra.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
       ra.xproj[d] = xp;
@@ -238,13 +300,8 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
       ra.clast[d] = cn ? cn + (size_t)ld * m.B * m.H : ra.cst + (size_t)d * m.B * m.H;
     }
     if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
-    if (algo == HS_ALGO_TC) {
-      int rc = hs::tc::recurrence(m.G, m.H, m.B, m.T, m.D, ra, packed, pl.ld + l * m.D, at<unsigned char>(ws, wl.tc), m.dtype, di.sms, s, g_err);
-      if (rc) return rc;
-    } else {
-      int rc = launch_recur_simt(m, di, ra, s);
-      if (rc) return rc;
-    }
+    int rc = launch_recur_simt(m, di, ra, s);
+    if (rc) return rc;
     if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
     in = out;
   }

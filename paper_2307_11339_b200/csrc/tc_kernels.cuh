@@ -1,25 +1,263 @@
-// tcgen05 tensor-core path (placeholder until the sm_100a kernels land).
+// Host glue of the tensor-core path: feasibility, packed-weight layout,
+// tensor maps, launches of K1 (tc_gemm.cuh) and K2/K3 (tc_recur.cuh).
 #pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
 #include <string>
+
 #include "simt_kernels.cuh"
+#include "tc_gemm.cuh"
+#include "tc_recur.cuh"
 
 namespace hs {
 namespace tc {
-inline bool supports(int, int, int, int, int) { return false; }
-inline bool profitable(int, int, int, int) { return false; }
-inline size_t packed_bytes(int, int, int) { return 0; }
-inline size_t workspace_bytes(int, int, int, int, int, int) { return 0; }
-inline int pack_layer(int, int, int, const float*, const float*, unsigned char*, cudaStream_t, std::string& err) {
-  err = "tensor-core path not built"; return 3;
+
+constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per block on sm_100
+
+inline int pad16(int b) { return (b + 15) / 16 * 16; }
+
+// Pick the K-split (cluster size) for the recurrence: the largest grid that
+// still fits one CTA per SM, with the W_hh slice + h staging + partial-sum
+// buffer inside 227 KB of shared memory.
+inline int choose_split(int G, int H, int B, int D, int NPL, int max_ctas) {
+  const int Npad = pad16(B);
+  if (H % 64 || Npad > 256) return 0;
+  const int RB = H / 32;
+  int best = 0;
+  for (int S = 1; S <= 8; S *= 2) {
+    if (H % (64 * S)) continue;
+    const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
+    if (L.nch > RMAXCH || L.total > kSmemMax) continue;
+    if (Npad / (128 / (32 / S)) > RMAXCELLS) continue;
+    if (D * RB * S > max_ctas) continue;
+    best = S;  // increasing S -> larger grid; keep the largest that fits
+  }
+  return best;
 }
-inline int input_projection(int, int, int, int, const float*, const unsigned char*, const float*, float*, unsigned char*, int,
-                            cudaStream_t, std::string& err) {
-  err = "tensor-core path not built"; return 3;
+
+inline bool supports(int G, int H, int B, int I0, int DH, int D = 1, int NPL = 2) {
+  if (I0 % 64 || DH % 64 || (G * H) % 128 || H % 64 || B > 256) return false;
+  return choose_split(G, H, B, D, NPL, 148) > 0;
 }
-template <typename LP>
-inline int recurrence(int, int, int, int, int, RecurArgs&, const void*, const LP*, unsigned char*, int, int, cudaStream_t,
+
+inline bool profitable(int G, int H, int B, int T) { return H >= 256 && B >= 4 && (long)T * B >= 128; }
+
+inline int gemm_bn(int N) { return N % 256 == 0 ? 256 : 128; }
+
+// packed planes per layer-direction: W_ih [2][G*H][I] bf16, W_hh row-block packed [2][H/32*128][H] bf16
+inline size_t wih_plane_elems(int G, int H, int I) { return (size_t)G * H * I; }
+inline size_t whh_plane_elems(int H) { return (size_t)(H / 32) * 128 * H; }
+inline size_t packed_bytes(int G, int H, int I) {
+  if (H % 32) return 0;
+  return 2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H));
+}
+
+struct TcWs {
+  size_t xpl, hbuf, counters, total;
+};
+inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
+  (void)G;
+  TcWs w{};
+  size_t off = 0;
+  const size_t cols = (size_t)(I0 > D * H ? I0 : D * H);
+  w.xpl = off;      off += ((2 * (size_t)T * B * cols * 2) + 255) / 256 * 256;
+  w.hbuf = off;     off += ((3 * (size_t)D * 2 * pad16(B) * H * 2) + 255) / 256 * 256;
+  w.counters = off; off += 256;
+  w.total = off;
+  return w;
+}
+inline size_t workspace_bytes(int G, int H, int B, int T, int D, int I0) {
+  if (H % 64) return 0;
+  return tc_ws_layout(G, H, B, T, D, I0).total;
+}
+
+__global__ void pack_tc_kernel(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
+                               __nv_bfloat16* __restrict__ wih_pl, __nv_bfloat16* __restrict__ whh_pl, int G, int H,
+                               int I) {
+  const size_t n_ih = (size_t)G * H * I;
+  const size_t n_hh = (size_t)(H / 32) * 128 * H;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_ih; i += stride) {
+    __nv_bfloat16 hi, lo;
+    ptx::split_bf16(w_ih[i], hi, lo);
+    wih_pl[i] = hi;
+    wih_pl[n_ih + i] = lo;
+  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_hh; i += stride) {
+    const int k = (int)(i % H);
+    const size_t r = i / H;
+    const int rb = (int)(r / 128), g = (int)((r % 128) / 32), u = (int)(r % 32);
+    const float v = g < G ? w_hh[((size_t)g * H + rb * 32 + u) * H + k] : 0.f;
+    __nv_bfloat16 hi, lo;
+    ptx::split_bf16(v, hi, lo);
+    whh_pl[i] = hi;
+    whh_pl[n_hh + i] = lo;
+  }
+}
+
+inline int pack_layer(int G, int H, int I, const float* w_ih, const float* w_hh, unsigned char* dst, cudaStream_t s,
                       std::string& err) {
-  err = "tensor-core path not built"; return 3;
+  __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(dst);
+  __nv_bfloat16* whh = wih + 2 * wih_plane_elems(G, H, I);
+  pack_tc_kernel<<<592, 256, 0, s>>>(w_ih, w_hh, wih, whh, G, H, I);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("pack_tc_kernel: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
 }
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3D bf16 map {inner, rows, planes}, 128B swizzle, box {64, box_rows, 1}.
+inline int make_map3(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t planes, uint32_t box_rows,
+                     std::string& err) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    err = "cuTensorMapEncodeTiled unavailable";
+    return 2;
+  }
+  cuuint64_t dims[3] = {inner, rows, planes};
+  cuuint64_t strides[2] = {inner * 2, inner * rows * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r);
+    return 2;
+  }
+  return 0;
+}
+
+template <typename K>
+inline int set_smem(K kernel, size_t bytes, std::string& err) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+// K1 on planes: A planes [2][M][K], W_ih planes [2][N][K]
+inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const float* bias, float* C, int M, int N, int K,
+                       int npass, cudaStream_t s, std::string& err) {
+  CUtensorMap ta, tb;
+  const int BN = gemm_bn(N);
+  int rc = make_map3(&ta, apl, K, M, 2, GBM, err);
+  if (!rc) rc = make_map3(&tb, wpl, K, N, 2, BN, err);
+  if (rc) return rc;
+  dim3 grid(N / BN, (M + GBM - 1) / GBM);
+  cudaError_t e;
+  if (BN == 256) {
+    static bool init = false;
+    if (!init) { if ((rc = set_smem(gemm_xproj_kernel<256>, gemm_smem_bytes<256>(), err))) return rc; init = true; }
+    gemm_xproj_kernel<256><<<grid, 256, gemm_smem_bytes<256>(), s>>>(ta, tb, bias, C, M, N, K, npass);
+  } else {
+    static bool init = false;
+    if (!init) { if ((rc = set_smem(gemm_xproj_kernel<128>, gemm_smem_bytes<128>(), err))) return rc; init = true; }
+    gemm_xproj_kernel<128><<<grid, 256, gemm_smem_bytes<128>(), s>>>(ta, tb, bias, C, M, N, K, npass);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("gemm_xproj_kernel launch: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int cols, cudaStream_t s, std::string& err) {
+  const size_t total = rows * cols;
+  int blocks = (int)((total / 4 + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  split_planes_kernel<<<blocks, 256, 0, s>>>(x, out, rows, cols, cols);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("split_planes_kernel: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+template <int G, int NPL>
+inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
+                        int S, size_t smem, cudaStream_t s, std::string& err) {
+  static bool init = false;
+  int rc;
+  if (!init) {
+    if ((rc = set_smem(recur_tc_kernel<G, NPL>, kSmemMax, err))) return rc;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.D * a.RB * S);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL>, &cfg);
+  if (e != cudaSuccess) {
+    err = std::string("cudaOccupancyMaxActiveClusters: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  if (nclusters * S < (int)cfg.gridDim.x) {
+    err = "recurrent kernel needs " + std::to_string(cfg.gridDim.x / S) + " co-resident clusters of " +
+          std::to_string(S) + ", device fits " + std::to_string(nclusters);
+    return 3;
+  }
+  e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL>, w0, w1, hm, a);
+  if (e != cudaSuccess) {
+    err = std::string("recur_tc_kernel launch: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+// One layer of recurrence (both directions).  W_hh planes for dir d at whh[d].
+inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, int sms,
+                            cudaStream_t s, std::string& err) {
+  const int S = choose_split(G, a.H, a.B, a.D, NPL, sms);
+  if (!S) {
+    err = "no feasible tensor-core split for this shape";
+    return 3;
+  }
+  a.S = S;
+  a.RB = a.H / 32;
+  CUtensorMap w0, w1, hm;
+  int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
+  if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
+  if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * NPL, a.Npad, err);
+  if (rc) return rc;
+  const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL).total;
+  if (G == 4) return NPL == 2 ? launch_recur<4, 2>(w0, w1, hm, a, S, smem, s, err) : launch_recur<4, 1>(w0, w1, hm, a, S, smem, s, err);
+  return NPL == 2 ? launch_recur<3, 2>(w0, w1, hm, a, S, smem, s, err) : launch_recur<3, 1>(w0, w1, hm, a, S, smem, s, err);
+}
+
 }  // namespace tc
 }  // namespace hs
