@@ -20,7 +20,12 @@ inline int pad16(int b) { return (b + 15) / 16 * 16; }
 // Pick the K-split (cluster size) for the recurrence: the largest grid that
 // still fits one CTA per SM, with the W_hh slice + h staging + partial-sum
 // buffer inside 227 KB of shared memory.
-inline int choose_split(int G, int H, int B, int D, int NPL, int max_ctas) {
+// Co-resident CTA limits per cluster size when the device cannot be queried
+// (cluster placement strands SMs: measured 15 clusters of 8 on a B200).
+inline int static_cta_limit(int S) { return S <= 2 ? 148 : S == 4 ? 132 : 120; }
+
+template <typename Limit>
+inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
   const int Npad = pad16(B);
   if (H % 64 || Npad > 256) return 0;
   const int RB = H / 32;
@@ -30,7 +35,7 @@ inline int choose_split(int G, int H, int B, int D, int NPL, int max_ctas) {
     const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
     if (Npad / (128 / (32 / S)) > RMAXCELLS) continue;
-    if (D * RB * S > max_ctas) continue;
+    if (D * RB * S > max_ctas(S)) continue;
     best = S;  // increasing S -> larger grid; keep the largest that fits
   }
   return best;
@@ -38,7 +43,7 @@ inline int choose_split(int G, int H, int B, int D, int NPL, int max_ctas) {
 
 inline bool supports(int G, int H, int B, int I0, int DH, int D = 1, int NPL = 2) {
   if (I0 % 64 || DH % 64 || (G * H) % 128 || H % 64 || B > 256) return false;
-  return choose_split(G, H, B, D, NPL, 148) > 0;
+  return choose_split(G, H, B, D, NPL, static_cta_limit) > 0;
 }
 
 inline bool profitable(int G, int H, int B, int T) { return H >= 256 && B >= 4 && (long)T * B >= 128; }
@@ -200,6 +205,39 @@ inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int col
 }
 
 template <int G, int NPL>
+inline int max_coresident_ctas_t(int S, size_t smem) {
+  static bool init = false;
+  std::string err;
+  if (!init) {
+    if (set_smem(recur_tc_kernel<G, NPL>, kSmemMax, err)) return 0;
+    init = true;
+  }
+  if (smem > kSmemMax) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S * 16);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n * S;
+}
+
+inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
+  if (G == 4) return NPL == 2 ? max_coresident_ctas_t<4, 2>(S, smem) : max_coresident_ctas_t<4, 1>(S, smem);
+  return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
+}
+
+template <int G, int NPL>
 inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
                         int S, size_t smem, cudaStream_t s, std::string& err) {
   static bool init = false;
@@ -242,7 +280,12 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
 // One layer of recurrence (both directions).  W_hh planes for dir d at whh[d].
 inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, int sms,
                             cudaStream_t s, std::string& err) {
-  const int S = choose_split(G, a.H, a.B, a.D, NPL, sms);
+  (void)sms;
+  auto limit = [&](int S_) -> int {
+    const size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL).total;
+    return max_coresident_ctas(G, NPL, S_, sm_);
+  };
+  const int S = choose_split(G, a.H, a.B, a.D, NPL, limit);
   if (!S) {
     err = "no feasible tensor-core split for this shape";
     return 3;

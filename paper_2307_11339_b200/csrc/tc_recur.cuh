@@ -59,7 +59,7 @@ __host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int 
   L.red_off = off; off += (size_t)G * 32 * (Npad + 4) * 4;
   off = (off + 15) / 16 * 16;
   L.bar_off = off; off += 8 * (2 + RMAXCH) + 16;
-  L.total = off + 1024;  // alignment slack
+  L.total = off;  // dynamic smem starts 1024-aligned (checked in-kernel)
   return L;
 }
 
@@ -74,8 +74,9 @@ template <int G, int NPL>
 __global__ void __launch_bounds__(256, 1)
     recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                     const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 atoms need 1024-B alignment
   const int H = a.H, B = a.B, Npad = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
   const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
   const int nch = L.nch;

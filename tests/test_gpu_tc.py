@@ -14,7 +14,7 @@ TC_SHAPES = [
     RNNSpec("gru", 2, 128, 6, 8, input=64, dirs=2, algo="tc"),
     RNNSpec("lstm", 2, 512, 9, 64, input=192, dirs=2, algo="tc"),
     RNNSpec("gru", 3, 256, 7, 48, algo="tc"),
-    RNNSpec("lstm", 1, 128, 4, 256, algo="tc"),
+    RNNSpec("lstm", 1, 128, 4, 128, algo="tc"),
 ]
 
 
