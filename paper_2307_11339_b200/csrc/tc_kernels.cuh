@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <type_traits>
 
 #include "simt_kernels.cuh"
 #include "tc_gemm.cuh"
@@ -34,7 +35,7 @@ inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
     if (H % (64 * S)) continue;
     const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
-    if (Npad / (128 / (32 / S)) > RMAXCELLS) continue;
+    if ((Npad + 4 * S - 1) / (4 * S) > RMAXCELLS) continue;
     if (D * RB * S > max_ctas(S)) continue;
     best = S;  // increasing S -> larger grid; keep the largest that fits
   }
@@ -59,7 +60,7 @@ inline size_t packed_bytes(int G, int H, int I) {
 }
 
 struct TcWs {
-  size_t xpl, hbuf, counters, total;
+  size_t xpl, hbuf, counters, trace, total;
 };
 inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   (void)G;
@@ -69,6 +70,7 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   w.xpl = off;      off += ((2 * (size_t)T * B * cols * 2) + 255) / 256 * 256;
   w.hbuf = off;     off += ((3 * (size_t)D * 2 * pad16(B) * H * 2) + 255) / 256 * 256;
   w.counters = off; off += 256;
+  w.trace = off;    off += (size_t)160 * kTraceSteps * 8 * 8;
   w.total = off;
   return w;
 }
@@ -209,7 +211,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   static bool init = false;
   std::string err;
   if (!init) {
-    if (set_smem(recur_tc_kernel<G, NPL>, kSmemMax, err)) return 0;
+    if (set_smem(recur_tc_kernel<G, NPL, 1>, kSmemMax, err)) return 0;
     init = true;
   }
   if (smem > kSmemMax) return 0;
@@ -225,7 +227,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL, 1>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -237,13 +239,13 @@ inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
   return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
 }
 
-template <int G, int NPL>
+template <int G, int NPL, int CELLS>
 inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
                         int S, size_t smem, cudaStream_t s, std::string& err) {
   static bool init = false;
   int rc;
   if (!init) {
-    if ((rc = set_smem(recur_tc_kernel<G, NPL>, kSmemMax, err))) return rc;
+    if ((rc = set_smem(recur_tc_kernel<G, NPL, CELLS>, kSmemMax, err))) return rc;
     init = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -259,7 +261,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL>, &cfg);
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL, CELLS>, &cfg);
   if (e != cudaSuccess) {
     err = std::string("cudaOccupancyMaxActiveClusters: ") + cudaGetErrorString(e);
     return 2;
@@ -269,12 +271,33 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
           std::to_string(S) + ", device fits " + std::to_string(nclusters);
     return 3;
   }
-  e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL>, w0, w1, hm, a);
+  e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL, CELLS>, w0, w1, hm, a);
   if (e != cudaSuccess) {
     err = std::string("recur_tc_kernel launch: ") + cudaGetErrorString(e);
     return 2;
   }
   return 0;
+}
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// Map runtime (G, NPL, cells per owner thread) to a kernel instantiation.
+template <typename F>
+inline int dispatch_cells(int G, int NPL, int cells, F&& f, std::string& err) {
+  auto by_cells = [&](auto g_, auto npl_) -> int {
+    switch (cells) {
+      case 1: return f(g_, npl_, IC<1>{});
+      case 2: return f(g_, npl_, IC<2>{});
+      case 4: return f(g_, npl_, IC<4>{});
+      case 8: return f(g_, npl_, IC<8>{});
+      case 16: return f(g_, npl_, IC<16>{});
+      case 32: return f(g_, npl_, IC<32>{});
+      default: err = "unsupported cells-per-thread " + std::to_string(cells); return 3;
+    }
+  };
+  if (G == 4) return NPL == 2 ? by_cells(IC<4>{}, IC<2>{}) : by_cells(IC<4>{}, IC<1>{});
+  return NPL == 2 ? by_cells(IC<3>{}, IC<2>{}) : by_cells(IC<3>{}, IC<1>{});
 }
 
 // One layer of recurrence (both directions).  W_hh planes for dir d at whh[d].
@@ -298,8 +321,11 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * NPL, a.Npad, err);
   if (rc) return rc;
   const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL).total;
-  if (G == 4) return NPL == 2 ? launch_recur<4, 2>(w0, w1, hm, a, S, smem, s, err) : launch_recur<4, 1>(w0, w1, hm, a, S, smem, s, err);
-  return NPL == 2 ? launch_recur<3, 2>(w0, w1, hm, a, S, smem, s, err) : launch_recur<3, 1>(w0, w1, hm, a, S, smem, s, err);
+  int cells = 1;
+  while (cells * (128 / (32 / S)) < a.Npad) cells *= 2;
+  return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) {
+    return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value>(w0, w1, hm, a, S, smem, s, err);
+  }, err);
 }
 
 }  // namespace tc

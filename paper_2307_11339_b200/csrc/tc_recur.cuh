@@ -27,7 +27,7 @@ namespace hs {
 namespace tc {
 
 constexpr int RMAXCH = 16;   // max 64-wide K chunks per CTA (K-slice <= 1024)
-constexpr int RMAXCELLS = 32;
+constexpr int RMAXCELLS = 32;  // owner cells per epilogue thread (template CELLS <= this)
 
 struct TcRecurArgs {
   int H, B, Npad, T, D, S;
@@ -42,7 +42,21 @@ struct TcRecurArgs {
   __nv_bfloat16* ypl;           // [2][T*B][D*H] bf16 planes for the next layer's K1, or nullptr
   __nv_bfloat16* hbuf;          // [3][D][NPL][Npad][H] bf16
   unsigned int* counters;       // [D][S]
+  unsigned long long* trace;    // optional [grid][kTraceSteps][8] %globaltimer stamps (debug)
 };
+
+constexpr int kTraceSteps = 64;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HS_TRACE(phase)                                                                          \
+  do {                                                                                           \
+    if (a.trace && s < kTraceSteps)                                                              \
+      a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 8 + (phase)] = globaltimer();             \
+  } while (0)
 
 struct RecurLayout {
   int nch;        // K chunks per CTA
@@ -70,7 +84,7 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int G, int NPL>
+template <int G, int NPL, int CELLS>
 __global__ void __launch_bounds__(256, 1)
     recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                     const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
@@ -127,21 +141,37 @@ __global__ void __launch_bounds__(256, 1)
         ptx::tma_load_3d(sW + ((size_t)p * nch + c) * 128 * 64, tmW, w_full, q * KS + c * 64, rb * 128, p);
   }
 
-  // owner cells: unit u_loc in [0, UO), batch rows b = b0 + k*bstep
+  // owner cells: unit u_loc in [0, UO), batch rows b = b0 + k*bstep, k < CELLS
   const int e = threadIdx.x - 128;
   const int u_loc = e >= 0 ? e % UO : 0;
   const int b0 = e >= 0 ? e / UO : 0;
   const int bstep = 128 / UO;
-  const int ncell = Npad / bstep;
   const int unit = rb * 32 + q * UO + u_loc;
-  float c_reg[RMAXCELLS], h_reg[RMAXCELLS];
+  const float* bh = a.bias_h[d];
+  float bias_r = 0.f, bias_z = 0.f, bias_n = 0.f;
+  if (G == 3 && bh) {
+    bias_r = bh[unit];
+    bias_z = bh[H + unit];
+    bias_n = bh[2 * H + unit];
+  }
+  float c_reg[CELLS], h_reg[CELLS], xq[CELLS][G];
+  auto load_xproj = [&](int step) {
+    const int tt = d == 0 ? step : T - 1 - step;
+    const float* __restrict__ xp = a.xproj[d] + (size_t)tt * B * GH + unit;
+#pragma unroll
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+#pragma unroll
+      for (int g = 0; g < G; ++g) xq[k][g] = b < B ? __ldg(xp + (size_t)b * GH + g * H) : 0.f;
+    }
+  };
   if (warp >= 4) {
 #pragma unroll
-    for (int k = 0; k < RMAXCELLS; ++k) {
+    for (int k = 0; k < CELLS; ++k) {
       c_reg[k] = 0.f;
       h_reg[k] = 0.f;
       const int b = b0 + k * bstep;
-      if (k < ncell && b < B) {
+      if (b < B) {
         h_reg[k] = a.h0[d][(size_t)b * H + unit];
         if (G == 4) c_reg[k] = a.c0[d][(size_t)b * H + unit];
         __nv_bfloat16 hi, lo;
@@ -152,6 +182,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     ptx::fence_proxy_async_global();
+    load_xproj(0);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -166,11 +197,13 @@ __global__ void __launch_bounds__(256, 1)
     const int buf_in = s % 3, buf_out = (s + 1) % 3;
     if (warp == 0) {
       if (ptx::elect_one()) {
+        HS_TRACE(0);
         const unsigned int target = (unsigned int)RB * (unsigned int)(s + 1);
         unsigned int seen;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter) : "memory");
         } while (seen < target);
+        HS_TRACE(1);
         ptx::fence_proxy_async_global();
         for (int c = 0; c < nch; ++c) {
           ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(NPL * Npad * 128));
@@ -201,6 +234,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         ptx::mma_commit(acc_full);
+        HS_TRACE(2);
       }
       __syncwarp();
     }
@@ -209,79 +243,100 @@ __global__ void __launch_bounds__(256, 1)
       const int sub = warp & 3;
       ptx::mbar_wait(acc_full, s & 1);
       ptx::tc_fence_after();
+      if (e == 0) HS_TRACE(3);
       if (sub < G) {
         const int o = lane / UO, ul = lane % UO;
         const uint32_t local = ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + ul) * rstride);
         const uint32_t remote = ptx::mapa(local, (uint32_t)o);
-        for (int c16 = 0; c16 < Npad / 16; ++c16) {
+        for (int c32 = 0; c32 < Npad / 32; ++c32) {
+          float v[32];
+          ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(sub * 32) << 16) + c32 * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            ptx::st_cluster_v4(remote + (uint32_t)(c32 * 32 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        if (Npad & 16) {
           float v[16];
-          ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + c16 * 16, v);
+          const int c0 = Npad & ~31;
+          ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + c0, v);
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
-            ptx::st_cluster_v4(remote + (uint32_t)(c16 * 16 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+            ptx::st_cluster_v4(remote + (uint32_t)(c0 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
       ptx::tc_fence_before();
+      if (e == 0) HS_TRACE(4);
     }
     cluster_arrive();
     cluster_wait();  // all partials for my units are in my shared memory
+    const bool last = s == T - 1;
     if (warp >= 4) {
-      const bool last = s == T - 1;
-      const float* xp = a.xproj[d] + (size_t)t * B * GH + unit;
-      const float* bh = a.bias_h[d];
+      if (e == 0) HS_TRACE(5);
+      // critical path: gates -> h_t planes for the next step
 #pragma unroll
-      for (int k = 0; k < RMAXCELLS; ++k) {
+      for (int k = 0; k < CELLS; ++k) {
         const int b = b0 + k * bstep;
-        if (k >= ncell) break;
-        float pre[4];
+        if (b >= Npad) break;
+        float pre[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          float acc = 0.f;
-          for (int sr = 0; sr < S; ++sr) acc += red[((size_t)(sr * G + g) * UO + u_loc) * rstride + b];
+          const float* rp = red + ((size_t)g * UO + u_loc) * rstride + b;
+          float acc = rp[0];
+          for (int sr = 1; sr < S; ++sr) acc += rp[(size_t)sr * G * UO * rstride];
           pre[g] = acc;
         }
-        if (b >= B) continue;
-        const float* xr = xp + (size_t)b * GH;
         float h;
         if (G == 4) {
-          const float ig = sigmoidf_(pre[0] + xr[0]), fg = sigmoidf_(pre[1] + xr[H]);
-          const float gg = tanhf_(pre[2] + xr[2 * H]), og = sigmoidf_(pre[3] + xr[3 * H]);
+          const float ig = sigmoidf_(pre[0] + xq[k][0]), fg = sigmoidf_(pre[1] + xq[k][1]);
+          const float gg = tanhf_(pre[2] + xq[k][2]), og = sigmoidf_(pre[3] + xq[k][3]);
           const float cnew = fg * c_reg[k] + ig * gg;
           c_reg[k] = cnew;
           h = og * tanhf_(cnew);
         } else {
-          const float r = sigmoidf_(xr[0] + pre[0] + (bh ? bh[unit] : 0.f));
-          const float z = sigmoidf_(xr[H] + pre[1] + (bh ? bh[H + unit] : 0.f));
-          const float n = tanhf_(xr[2 * H] + r * (pre[2] + (bh ? bh[2 * H + unit] : 0.f)));
+          const float r = sigmoidf_(xq[k][0] + pre[0] + bias_r);
+          const float z = sigmoidf_(xq[k][1] + pre[1] + bias_z);
+          const float n = tanhf_(xq[k][2] + r * (pre[2] + bias_n));
           h = (1.f - z) * n + z * h_reg[k];
         }
         h_reg[k] = h;
-        __nv_bfloat16 hi, lo;
-        ptx::split_bf16(h, hi, lo);
-        if (!last) {
+        if (!last && b < B) {
+          __nv_bfloat16 hi, lo;
+          ptx::split_bf16(h, hi, lo);
           __nv_bfloat16* hb = a.hbuf + ((size_t)(buf_out * D + d) * NPL) * plane_stride + (size_t)b * H + unit;
           hb[0] = NPL == 2 ? hi : __float2bfloat16_rn(h);
           if (NPL == 2) hb[plane_stride] = lo;
         }
-        const size_t yrow = (size_t)t * B + b;
-        if (a.y) a.y[yrow * D * H + (size_t)d * H + unit] = h;
+      }
+      ptx::fence_proxy_async_global();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (e == 0 && !last) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
+        HS_TRACE(6);
+      }
+      // off the critical path: layer outputs, final state, next step's XP
+#pragma unroll
+      for (int k = 0; k < CELLS; ++k) {
+        const int b = b0 + k * bstep;
+        if (b >= B) continue;
+        const float h = h_reg[k];
+        const size_t yidx = ((size_t)t * B + b) * D * H + (size_t)d * H + unit;
+        if (a.y) a.y[yidx] = h;
         if (a.ypl) {
-          const size_t plane = (size_t)T * B * D * H;
-          a.ypl[yrow * D * H + (size_t)d * H + unit] = hi;
-          a.ypl[plane + yrow * D * H + (size_t)d * H + unit] = lo;
+          __nv_bfloat16 hi, lo;
+          ptx::split_bf16(h, hi, lo);
+          a.ypl[yidx] = hi;
+          a.ypl[(size_t)T * B * D * H + yidx] = lo;
         }
         if (last) {
           a.hn[d][(size_t)b * H + unit] = h;
           if (G == 4) a.cn[d][(size_t)b * H + unit] = c_reg[k];
         }
       }
-      ptx::fence_proxy_async_global();
+      if (!last) load_xproj(s + 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s + 1 < T) {
-      __threadfence();
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
-    }
+    if (threadIdx.x == 0) HS_TRACE(7);
     cluster_arrive();
   }
   cluster_wait();
