@@ -11,6 +11,12 @@ namespace hs {
 __device__ __forceinline__ float sigmoidf_(float v) { return 1.0f / (1.0f + expf(-v)); }
 __device__ __forceinline__ float tanhf_(float v) { return tanhf(v); }
 
+// Short-latency forms for the tensor-core epilogue (on the per-step critical
+// path): ex2.approx has ~2 ulp relative error, so sigmoid/tanh built on it
+// stay within ~1e-7 absolute — far below the 1e-4 budget.
+__device__ __forceinline__ float sigmoid_fast(float v) { return __fdividef(1.0f, 1.0f + __expf(-v)); }
+__device__ __forceinline__ float tanh_fast(float v) { return 1.0f - __fdividef(2.0f, __expf(2.0f * v) + 1.0f); }
+
 // Grid barrier for persistent kernels.  `ctr` is zeroed by the host before
 // the launch; round r (0-based) completes when every CTA has arrived r+1
 // times.  All CTAs must be co-resident (cooperative launch enforces it).

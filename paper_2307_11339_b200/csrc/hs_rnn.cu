@@ -249,13 +249,13 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     a.counters = counters;
     static const char* trace_path = getenv("HS_RECUR_TRACE");
     a.trace = trace_path && l == 0 ? reinterpret_cast<unsigned long long*>(tcws + tw.trace) : nullptr;
-    if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 8 * 8, s));
+    if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
     HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
-    HS_CUDA(cudaMemsetAsync(counters, 0, 256, s));
+    HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
     rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
     if (rc) return rc;
     if (a.trace) {
-      static unsigned long long host[160 * kTraceSteps * 8];
+      static unsigned long long host[160 * kTraceSteps * 16];
       HS_CUDA(cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s));
       HS_CUDA(cudaStreamSynchronize(s));
       FILE* f = fopen(trace_path, "wb");

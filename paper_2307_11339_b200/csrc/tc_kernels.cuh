@@ -35,7 +35,7 @@ inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
     if (H % (64 * S)) continue;
     const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
-    if ((Npad + 4 * S - 1) / (4 * S) > RMAXCELLS) continue;
+    if ((Npad + 8 * S - 1) / (8 * S) > RMAXCELLS) continue;
     if (D * RB * S > max_ctas(S)) continue;
     best = S;  // increasing S -> larger grid; keep the largest that fits
   }
@@ -69,8 +69,8 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   const size_t cols = (size_t)(I0 > D * H ? I0 : D * H);
   w.xpl = off;      off += ((2 * (size_t)T * B * cols * 2) + 255) / 256 * 256;
   w.hbuf = off;     off += ((3 * (size_t)D * 2 * pad16(B) * H * 2) + 255) / 256 * 256;
-  w.counters = off; off += 256;
-  w.trace = off;    off += (size_t)160 * kTraceSteps * 8 * 8;
+  w.counters = off; off += 128 * 128;  // <= 128 chunk counters, one 128-B line each
+  w.trace = off;    off += (size_t)160 * kTraceSteps * 16 * 8;
   w.total = off;
   return w;
 }
@@ -217,7 +217,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   if (smem > kSmemMax) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S * 16);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kRecurThreads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -250,7 +250,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.D * a.RB * S);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kRecurThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -322,7 +322,7 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   if (rc) return rc;
   const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL).total;
   int cells = 1;
-  while (cells * (128 / (32 / S)) < a.Npad) cells *= 2;
+  while (cells * (kEpiThreads / (32 / S)) < a.Npad) cells *= 2;
   return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) {
     return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value>(w0, w1, hm, a, S, smem, s, err);
   }, err);

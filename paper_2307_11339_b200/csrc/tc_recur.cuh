@@ -42,7 +42,7 @@ struct TcRecurArgs {
   __nv_bfloat16* ypl;           // [2][T*B][D*H] bf16 planes for the next layer's K1, or nullptr
   __nv_bfloat16* hbuf;          // [3][D][NPL][Npad][H] bf16
   unsigned int* counters;       // [D][S]
-  unsigned long long* trace;    // optional [grid][kTraceSteps][8] %globaltimer stamps (debug)
+  unsigned long long* trace;    // optional [grid][kTraceSteps][16] %globaltimer stamps (debug)
 };
 
 constexpr int kTraceSteps = 64;
@@ -55,7 +55,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #define HS_TRACE(phase)                                                                          \
   do {                                                                                           \
     if (a.trace && s < kTraceSteps)                                                              \
-      a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 8 + (phase)] = globaltimer();             \
+      a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 16 + (phase)] = globaltimer();             \
   } while (0)
 
 struct RecurLayout {
@@ -72,7 +72,7 @@ __host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int 
   L.h_off = off;   off += (size_t)NPL * L.nch * Npad * 128;
   L.red_off = off; off += (size_t)G * 32 * (Npad + 4) * 4;
   off = (off + 15) / 16 * 16;
-  L.bar_off = off; off += 8 * (2 + RMAXCH) + 16;
+  L.bar_off = off; off += 8 * (5 + RMAXCH) + 16;
   L.total = off;  // dynamic smem starts 1024-aligned (checked in-kernel)
   return L;
 }
@@ -80,12 +80,30 @@ __host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int 
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
+// arrive without release: used once this CTA's reads of the partial-sum
+// buffer have completed (their values are already consumed in registers)
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// One CTA = 8 warps.  Roles inside a timestep:
+//   warp 0 lane 0  producer: polls the per-chunk readiness counters of its
+//                  K-slice in order and TMA-loads each h chunk once published
+//   warp 1 lane 0  MMA issuer: tcgen05.mma per landed chunk, commit -> acc_full
+//   warp 2         TMEM allocator
+//   all 8 warps    drain TMEM (warp w reads lane quarter w%4; warps w, w+4
+//                  split the columns), reduce-scatter partial gates to the unit
+//                  owners over DSMEM, cluster barrier, then finish the gates of
+//                  the CTA's own units (c, h in registers), publish h_t planes
+//                  and release the chunk counter.
+constexpr int kRecurThreads = 256;
+constexpr int kEpiThreads = 256;
+
 template <int G, int NPL, int CELLS>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kRecurThreads, 1)
     recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                     const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -102,8 +120,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* w_full = bars;
   uint64_t* acc_full = bars + 1;
-  uint64_t* h_full = bars + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + RMAXCH);
+  uint64_t* h_full = bars + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + RMAXCH);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = (int)ptx::cluster_rank();
@@ -114,9 +132,13 @@ __global__ void __launch_bounds__(256, 1)
   const int GH = G * H;
   const int rstride = Npad + 4;
   const uint32_t tcols = Npad <= 32 ? 32 : Npad <= 64 ? 64 : Npad <= 128 ? 128 : 256;
-  const int own_slice = (rb * 32) / KS;
-  unsigned int* my_counter = a.counters + d * S + own_slice;
-  const unsigned int* in_counter = a.counters + d * S + q;
+  // readiness counters, one per 64-unit chunk of h (= 2 row blocks = 2S producer
+  // CTAs), each on its own 128-B line
+  constexpr int kCtrStride = 32;
+  const int nchunk_all = H / 64;
+  unsigned int* my_counter = a.counters + (d * nchunk_all + (rb * 32) / 64) * kCtrStride;
+  const unsigned int* in_counter = a.counters + (d * nchunk_all + (q * KS) / 64) * kCtrStride;
+  const unsigned int per_round = 2u * (unsigned int)S;
   const size_t plane_stride = (size_t)Npad * H;  // elements per (buf, d, plane) slab of hbuf
 
   if (warp == 0 && lane == 0) {
@@ -140,21 +162,21 @@ __global__ void __launch_bounds__(256, 1)
       for (int c = 0; c < nch; ++c)
         ptx::tma_load_3d(sW + ((size_t)p * nch + c) * 128 * 64, tmW, w_full, q * KS + c * 64, rb * 128, p);
   }
+  __syncwarp();
 
   // owner cells: unit u_loc in [0, UO), batch rows b = b0 + k*bstep, k < CELLS
-  const int e = threadIdx.x - 128;
-  const int u_loc = e >= 0 ? e % UO : 0;
-  const int b0 = e >= 0 ? e / UO : 0;
-  const int bstep = 128 / UO;
+  const int e = threadIdx.x;
+  const int u_loc = e % UO;
+  const int b0 = e / UO;
+  const int bstep = kEpiThreads / UO;
   const int unit = rb * 32 + q * UO + u_loc;
-  const float* bh = a.bias_h[d];
-  float bias_r = 0.f, bias_z = 0.f, bias_n = 0.f;
-  if (G == 3 && bh) {
-    bias_r = bh[unit];
-    bias_z = bh[H + unit];
-    bias_n = bh[2 * H + unit];
-  }
   float c_reg[CELLS], h_reg[CELLS], xq[CELLS][G];
+  float bias_r = 0.f, bias_z = 0.f, bias_n = 0.f;
+  if (G == 3 && a.bias_h[d]) {
+    bias_r = a.bias_h[d][unit];
+    bias_z = a.bias_h[d][H + unit];
+    bias_n = a.bias_h[d][2 * H + unit];
+  }
   auto load_xproj = [&](int step) {
     const int tt = d == 0 ? step : T - 1 - step;
     const float* __restrict__ xp = a.xproj[d] + (size_t)tt * B * GH + unit;
@@ -165,47 +187,52 @@ __global__ void __launch_bounds__(256, 1)
       for (int g = 0; g < G; ++g) xq[k][g] = b < B ? __ldg(xp + (size_t)b * GH + g * H) : 0.f;
     }
   };
-  if (warp >= 4) {
 #pragma unroll
-    for (int k = 0; k < CELLS; ++k) {
-      c_reg[k] = 0.f;
-      h_reg[k] = 0.f;
-      const int b = b0 + k * bstep;
-      if (b < B) {
-        h_reg[k] = a.h0[d][(size_t)b * H + unit];
-        if (G == 4) c_reg[k] = a.c0[d][(size_t)b * H + unit];
-        __nv_bfloat16 hi, lo;
-        ptx::split_bf16(h_reg[k], hi, lo);
-        __nv_bfloat16* hb = a.hbuf + ((size_t)(0 * D + d) * NPL) * plane_stride + (size_t)b * H + unit;
-        hb[0] = NPL == 2 ? hi : __float2bfloat16_rn(h_reg[k]);
-        if (NPL == 2) hb[plane_stride] = lo;
-      }
+  for (int k = 0; k < CELLS; ++k) {
+    c_reg[k] = 0.f;
+    h_reg[k] = 0.f;
+    const int b = b0 + k * bstep;
+    if (b < B) {
+      h_reg[k] = a.h0[d][(size_t)b * H + unit];
+      if (G == 4) c_reg[k] = a.c0[d][(size_t)b * H + unit];
+      __nv_bfloat16 hi, lo;
+      ptx::split_bf16(h_reg[k], hi, lo);
+      __nv_bfloat16* hb = a.hbuf + ((size_t)(0 * D + d) * NPL) * plane_stride + (size_t)b * H + unit;
+      hb[0] = NPL == 2 ? hi : __float2bfloat16_rn(h_reg[k]);
+      if (NPL == 2) hb[plane_stride] = lo;
     }
-    ptx::fence_proxy_async_global();
-    load_xproj(0);
   }
+  ptx::fence_proxy_async_global();
+  load_xproj(0);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
-  }
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
   cluster_arrive();
 
   const uint32_t idesc = ptx::idesc_bf16_f32(128, Npad);
+  const int sub = warp & 3;  // TMEM lane quarter
+  const bool split = (Npad % 32) == 0;
+  const int ncol = split ? Npad / 2 : Npad;
+  const int col0 = split ? (warp >> 2) * ncol : 0;
+  const bool active = sub < G && (split || warp >= 4);
+  const uint32_t red_remote =
+      ptx::mapa(ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride), (uint32_t)(lane / UO));
+
   for (int s = 0; s < T; ++s) {
     const int t = d == 0 ? s : T - 1 - s;
     const int buf_in = s % 3, buf_out = (s + 1) % 3;
+    const bool last = s == T - 1;
     if (warp == 0) {
-      if (ptx::elect_one()) {
+      if (lane == 0) {
         HS_TRACE(0);
-        const unsigned int target = (unsigned int)RB * (unsigned int)(s + 1);
-        unsigned int seen;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter) : "memory");
-        } while (seen < target);
-        HS_TRACE(1);
-        ptx::fence_proxy_async_global();
+        const unsigned int target = per_round * (unsigned int)(s + 1);
         for (int c = 0; c < nch; ++c) {
+          unsigned int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter + c * kCtrStride) : "memory");
+          } while (seen < target);
+          if (c == 0) HS_TRACE(1);
+          if (c == nch - 1) HS_TRACE(12);
+          ptx::fence_proxy_async_global();
           ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(NPL * Npad * 128));
           for (int p = 0; p < NPL; ++p)
             ptx::tma_load_3d(sH + ((size_t)p * nch + c) * Npad * 64, &tmH, &h_full[c], q * KS + c * 64, 0,
@@ -216,9 +243,12 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
       if (ptx::elect_one()) {
         if (s == 0) ptx::mbar_wait(w_full, 0);
+        HS_TRACE(13);
         for (int c = 0; c < nch; ++c) {
           ptx::mbar_wait(&h_full[c], s & 1);
           ptx::tc_fence_after();
+          if (c == 0) HS_TRACE(15);
+          if (c == nch - 1) HS_TRACE(14);
           const __nv_bfloat16* wh = sW + (size_t)c * 128 * 64;
           const __nv_bfloat16* hh = sH + (size_t)c * Npad * 64;
 #pragma unroll
@@ -239,105 +269,90 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
     }
     cluster_wait();  // peers finished reading last step's partials
-    if (warp >= 4) {
-      const int sub = warp & 3;
-      ptx::mbar_wait(acc_full, s & 1);
-      ptx::tc_fence_after();
-      if (e == 0) HS_TRACE(3);
-      if (sub < G) {
-        const int o = lane / UO, ul = lane % UO;
-        const uint32_t local = ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + ul) * rstride);
-        const uint32_t remote = ptx::mapa(local, (uint32_t)o);
-        for (int c32 = 0; c32 < Npad / 32; ++c32) {
-          float v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(sub * 32) << 16) + c32 * 32, v);
+    // 1. drain TMEM, reduce-scatter partial gates to the unit owners
+    ptx::mbar_wait(acc_full, s & 1);
+    ptx::tc_fence_after();
+    if (e == 128) HS_TRACE(3);
+    if (active) {
+      for (int c16 = 0; c16 < ncol / 16; ++c16) {
+        float v[16];
+        const int col = col0 + c16 * 16;
+        ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + col, v);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            ptx::st_cluster_v4(remote + (uint32_t)(c32 * 32 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-        if (Npad & 16) {
-          float v[16];
-          const int c0 = Npad & ~31;
-          ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + c0, v);
-#pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            ptx::st_cluster_v4(remote + (uint32_t)(c0 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
+        for (int j = 0; j < 16; j += 4)
+          ptx::st_cluster_v4(red_remote + (uint32_t)(col + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
       }
-      ptx::tc_fence_before();
-      if (e == 0) HS_TRACE(4);
     }
+    ptx::tc_fence_before();
+    if (e == 128) HS_TRACE(4);
     cluster_arrive();
     cluster_wait();  // all partials for my units are in my shared memory
-    const bool last = s == T - 1;
-    if (warp >= 4) {
-      if (e == 0) HS_TRACE(5);
-      // critical path: gates -> h_t planes for the next step
+    if (e == 128) HS_TRACE(5);
+    // 2. owner: gates -> h_t planes (critical path)
 #pragma unroll
-      for (int k = 0; k < CELLS; ++k) {
-        const int b = b0 + k * bstep;
-        if (b >= Npad) break;
-        float pre[G];
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+      if (b >= Npad) break;
+      float pre[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float* rp = red + ((size_t)g * UO + u_loc) * rstride + b;
-          float acc = rp[0];
-          for (int sr = 1; sr < S; ++sr) acc += rp[(size_t)sr * G * UO * rstride];
-          pre[g] = acc;
-        }
-        float h;
-        if (G == 4) {
-          const float ig = sigmoidf_(pre[0] + xq[k][0]), fg = sigmoidf_(pre[1] + xq[k][1]);
-          const float gg = tanhf_(pre[2] + xq[k][2]), og = sigmoidf_(pre[3] + xq[k][3]);
-          const float cnew = fg * c_reg[k] + ig * gg;
-          c_reg[k] = cnew;
-          h = og * tanhf_(cnew);
-        } else {
-          const float r = sigmoidf_(xq[k][0] + pre[0] + bias_r);
-          const float z = sigmoidf_(xq[k][1] + pre[1] + bias_z);
-          const float n = tanhf_(xq[k][2] + r * (pre[2] + bias_n));
-          h = (1.f - z) * n + z * h_reg[k];
-        }
-        h_reg[k] = h;
-        if (!last && b < B) {
-          __nv_bfloat16 hi, lo;
-          ptx::split_bf16(h, hi, lo);
-          __nv_bfloat16* hb = a.hbuf + ((size_t)(buf_out * D + d) * NPL) * plane_stride + (size_t)b * H + unit;
-          hb[0] = NPL == 2 ? hi : __float2bfloat16_rn(h);
-          if (NPL == 2) hb[plane_stride] = lo;
-        }
-      }
-      ptx::fence_proxy_async_global();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (e == 0 && !last) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
-        HS_TRACE(6);
-      }
-      // off the critical path: layer outputs, final state, next step's XP
+      for (int g = 0; g < G; ++g) {
+        const float* rp = red + ((size_t)g * UO + u_loc) * rstride + b;
+        float acc = rp[0];
 #pragma unroll
-      for (int k = 0; k < CELLS; ++k) {
-        const int b = b0 + k * bstep;
-        if (b >= B) continue;
-        const float h = h_reg[k];
-        const size_t yidx = ((size_t)t * B + b) * D * H + (size_t)d * H + unit;
-        if (a.y) a.y[yidx] = h;
-        if (a.ypl) {
-          __nv_bfloat16 hi, lo;
-          ptx::split_bf16(h, hi, lo);
-          a.ypl[yidx] = hi;
-          a.ypl[(size_t)T * B * D * H + yidx] = lo;
-        }
-        if (last) {
-          a.hn[d][(size_t)b * H + unit] = h;
-          if (G == 4) a.cn[d][(size_t)b * H + unit] = c_reg[k];
-        }
+        for (int sr = 1; sr < 8; ++sr)
+          if (sr < S) acc += rp[(size_t)sr * G * UO * rstride];
+        pre[g] = acc;
       }
-      if (!last) load_xproj(s + 1);
+      float h;
+      if (G == 4) {
+        const float ig = sigmoid_fast(pre[0] + xq[k][0]), fg = sigmoid_fast(pre[1] + xq[k][1]);
+        const float gg = tanh_fast(pre[2] + xq[k][2]), og = sigmoid_fast(pre[3] + xq[k][3]);
+        const float cnew = fg * c_reg[k] + ig * gg;
+        c_reg[k] = cnew;
+        h = og * tanh_fast(cnew);
+      } else {
+        const float r = sigmoid_fast(xq[k][0] + pre[0] + bias_r);
+        const float z = sigmoid_fast(xq[k][1] + pre[1] + bias_z);
+        const float n = tanh_fast(xq[k][2] + r * (pre[2] + bias_n));
+        h = (1.f - z) * n + z * h_reg[k];
+      }
+      h_reg[k] = h;
+      if (!last && b < B) {
+        __nv_bfloat16 hi, lo;
+        ptx::split_bf16(h, hi, lo);
+        __nv_bfloat16* hb = a.hbuf + ((size_t)(buf_out * D + d) * NPL) * plane_stride + (size_t)b * H + unit;
+        hb[0] = NPL == 2 ? hi : __float2bfloat16_rn(h);
+        if (NPL == 2) hb[plane_stride] = lo;
+      }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) HS_TRACE(7);
-    cluster_arrive();
+    if (e == 128) HS_TRACE(6);
+    cluster_arrive_relaxed();  // partial-sum buffer fully read: peers may refill it
+    ptx::fence_proxy_async_global();
+    __syncthreads();  // all h_t stores of this CTA issued
+    if (e == 128) HS_TRACE(8);
+    if (e == 0 && !last) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
+    if (e == 0) HS_TRACE(10);
+    // 3. off the critical path: layer outputs, final state, next step's XP
+#pragma unroll
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+      if (b >= B) continue;
+      const float hv = h_reg[k];
+      const size_t yidx = ((size_t)t * B + b) * D * H + (size_t)d * H + unit;
+      if (a.y) a.y[yidx] = hv;
+      if (a.ypl) {
+        __nv_bfloat16 hi, lo;
+        ptx::split_bf16(hv, hi, lo);
+        a.ypl[yidx] = hi;
+        a.ypl[(size_t)T * B * D * H + yidx] = lo;
+      }
+      if (last) {
+        a.hn[d][(size_t)b * H + unit] = hv;
+        if (G == 4) a.cn[d][(size_t)b * H + unit] = c_reg[k];
+      }
+    }
+    if (!last) load_xproj(s + 1);
+    if (e == 0) HS_TRACE(11);
   }
   cluster_wait();
   ptx::tc_fence_before();
