@@ -70,6 +70,8 @@ from .planner import (
     topo_sort_hybrid,
 )
 from .rnn import CONFIGS, RNNExecutor, RNNSpec, init_weights, load_library, make_input
+from .executor import ExecResult, HostRNN, build_schedule, execute, measure_link_bandwidth, profile_ops
+from .serve import InferenceRequest, InferenceResponse, RNNServer, register_model, run
 
 __all__ = [
     "__version__",
@@ -89,4 +91,6 @@ __all__ = [
     "baseline_plans", "gpu_plan_memory", "trace_to_csv", "save_trace",
     # B200 executor
     "RNNSpec", "CONFIGS", "RNNExecutor", "init_weights", "make_input", "load_library",
+    "HostRNN", "ExecResult", "build_schedule", "execute", "profile_ops", "measure_link_bandwidth",
+    "InferenceRequest", "InferenceResponse", "RNNServer", "register_model", "run",
 ]
