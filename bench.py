@@ -162,6 +162,40 @@ def torch_cpu_reference(spec, sample_batch, reps=3):
     return {"value": sample_batch / p50, "p50_ms": p50 * 1e3, "threads": torch.get_num_threads()}
 
 
+def time_planner(mod, spec, reps=3):
+    """Planner leg of the path on the spec's grid:
+    gen_lstm_grid + synth_profile(cpu-comparable, seed 0) + topo_sort_hybrid +
+    select_devices(alpha=0) + evaluate + simulate, median ms over ``reps``."""
+    graph, costmodel, planner, engine = mod.graph, mod.costmodel, mod.planner, mod.engine
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        g = graph.gen_lstm_grid(spec.layers, spec.seq)
+        cm = costmodel.synth_profile(g, costmodel.PRESETS["cpu-comparable"], 0)
+        order = planner.topo_sort_hybrid(g, cm)
+        plan = planner.select_devices(g, cm, order, 0.0)
+        ev = engine.evaluate(g, cm, plan)
+        tr = engine.simulate(g, cm, plan)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return {"ms": statistics.median(ts), "latency_ms": ev.latency, "makespan_ms": tr.makespan, "k_star": plan.k_star,
+            "n": g.n}
+
+
+def reference_planner():
+    """The unmodified reference package from baseline/_ref (None if absent)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "hetsched").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import hetsched
+        from hetsched import costmodel, engine, graph, planner  # noqa: F401
+
+        return hetsched
+    except Exception:
+        return None
+
+
 def run_reference(args, spec):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -192,6 +226,9 @@ def run_reference(args, spec):
                          "host": info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    hs = reference_planner()
+    if hs is not None:
+        line["reference_planner"] = dict(time_planner(hs, spec), package=f"hetsched {hs.__version__} (baseline/_ref)")
     print(json.dumps(line), flush=True)
     return 0
 
@@ -329,6 +366,10 @@ def main(argv=None):
         "gpu_launches": ex.launches_per_forward() * args.steps,
         "clocks": clocks.summary(),
     }
+    if world == 1:
+        import paper_2307_11339_b200 as pkg
+
+        line["planner"] = dict(time_planner(pkg, spec), note="this package's planner (bit-exact with the reference)")
     if world == 1 and not args.no_cpu_baseline:
         info = cpu_info()
         cb = time_cpu_baseline(spec, args.cpu_baseline_seconds, args.cpu_sample_batch)
