@@ -108,6 +108,25 @@ int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed,
                           void* workspace, size_t ws_bytes, void* stream,
                           float* layer_ms);
 
+/* End-to-end forward on HOST buffers (the request path; pinned host memory
+ * gives asynchronous copies).  x_host [T,B,I], h0_host/c0_host
+ * [L*D,B,H] or NULL, outputs y_host [T,B,D*H], hn_host/cn_host [L*D,B,H].
+ * x_dev/y_dev/hn_dev/cn_dev are caller-owned device staging buffers of the
+ * same shapes; state_dev ([2][L*D,B,H], may be NULL without initial states)
+ * stages h0/c0.  On the tensor-core path the copies overlap the compute: x is
+ * uploaded in time chunks on an internal copy stream and each chunk's
+ * layer-0 input projection starts when it lands; y is downloaded in time
+ * chunks while the last layer's recurrence still runs (the copy stream
+ * waits on per-step progress counters the kernel publishes).  All work,
+ * copies included, is complete when `stream` reaches the end of the call.
+ * Replaces: engine.simulate with io_transfers=True (engine.py:128-137,
+ * 296-299, 375-378) — the host staging of entry inputs / exit outputs. */
+int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed,
+                        const void* x_host, const void* h0_host, const void* c0_host,
+                        void* y_host, void* hn_host, void* cn_host,
+                        void* x_dev, void* y_dev, void* hn_dev, void* cn_dev, void* state_dev,
+                        void* workspace, size_t ws_bytes, void* stream);
+
 /* Convenience: pack + forward (weights in PyTorch layout).  Needs
  * packed_size + workspace bytes of workspace. */
 int hs_rnn_forward(const hs_rnn_desc* desc, const void* x,

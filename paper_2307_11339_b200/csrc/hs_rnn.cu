@@ -198,12 +198,65 @@ int launch_recur_simt(const Dims& m, const DeviceInfo& di, hs::RecurArgs& ra, cu
 }
 
 
+// ------------------------------------------------ host-buffer forward support
+// Copies overlapped with compute (hs_rnn_forward_host): x is uploaded in time
+// chunks on a copy stream and each chunk's layer-0 input projection starts as
+// soon as it lands; y is drained in time chunks while the last layer's
+// recurrence is still running (the copy stream waits on per-step progress
+// counters the kernel publishes, via cuStreamWaitValue32).
+struct Overlap {
+  const float* x_host = nullptr;
+  float* y_host = nullptr;
+  cudaStream_t cs = nullptr;
+};
+
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn wait_value_fn() {
+  static WaitValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValue32Fn>(p);
+    if (getenv("HS_DEBUG")) fprintf(stderr, "[hsrnn] cuStreamWaitValue32 %s\n", fn ? "available" : "unavailable");
+  }
+  return fn;
+}
+
+int copy_stream(cudaStream_t* out) {
+  static thread_local cudaStream_t cache[16] = {};
+  int dev;
+  HS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
+  if (!cache[dev]) HS_CUDA(cudaStreamCreateWithFlags(&cache[dev], cudaStreamNonBlocking));
+  *out = cache[dev];
+  return HS_OK;
+}
+
+// s2 waits for all work enqueued on s1 so far
+int join(cudaStream_t s1, cudaStream_t s2) {
+  cudaEvent_t ev;
+  HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  HS_CUDA(cudaEventRecord(ev, s1));
+  HS_CUDA(cudaStreamWaitEvent(s2, ev, 0));
+  HS_CUDA(cudaEventDestroy(ev));
+  return HS_OK;
+}
+
+inline void chunk_bounds(int T, int n, int k, int* t0, int* t1) {
+  *t0 = (int)((long)T * k / n);
+  *t1 = (int)((long)T * (k + 1) / n);
+}
+
 // Tensor-core forward: per layer, split the input into bf16 planes (layer 0;
 // later layers get their planes straight from the previous recurrence
 // epilogue), K1 GEMM per direction, then one recurrent launch (both dirs).
 int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const void* packed, const float* x,
                const float* h0, const float* c0, float* y, float* hn, float* cn, void* ws, const WsLayout& wl,
-               cudaStream_t s, float* layer_ms) {
+               cudaStream_t s, float* layer_ms, const Overlap* ov = nullptr) {
   using namespace hs::tc;
   const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
   const size_t TB = (size_t)m.T * m.B;
@@ -219,8 +272,41 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   const int nev = layer_ms ? 2 * m.L + 1 : 0;
   for (int i = 0; i < nev; ++i) HS_CUDA(cudaEventCreate(&evs[i]));
   if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
-  int rc = split_planes(x, xpl, TB, m.I, s, g_err);
-  if (rc) return rc;
+  int rc;
+  const bool chunked_in = ov && ov->x_host;
+  if (chunked_in) {
+    // upload x in time chunks on the copy stream; split + layer-0 K1 per chunk
+    const int nci = m.T < 16 ? m.T : 16;
+    if ((rc = join(s, ov->cs))) return rc;  // x staging is free once earlier work on s is done
+    cudaEvent_t ev_in[16];
+    for (int k = 0; k < nci; ++k) {
+      int t0, t1;
+      chunk_bounds(m.T, nci, k, &t0, &t1);
+      const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
+      HS_CUDA(cudaMemcpyAsync(const_cast<float*>(x) + r0 * m.I, ov->x_host + r0 * m.I, nr * m.I * sizeof(float),
+                              cudaMemcpyHostToDevice, ov->cs));
+      HS_CUDA(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+      HS_CUDA(cudaEventRecord(ev_in[k], ov->cs));
+    }
+    for (int k = 0; k < nci; ++k) {
+      int t0, t1;
+      chunk_bounds(m.T, nci, k, &t0, &t1);
+      const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
+      HS_CUDA(cudaStreamWaitEvent(s, ev_in[k], 0));
+      HS_CUDA(cudaEventDestroy(ev_in[k]));
+      if ((rc = split_planes(x + r0 * m.I, xpl + r0 * m.I, nr, m.I, s, g_err, TB * m.I))) return rc;
+      for (int d = 0; d < m.D; ++d) {
+        const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, pl.ld[d].tc);
+        float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
+        rc = gemm_planes(xpl + r0 * m.I, wih, at<float>(packed, pl.ld[d].bias_x), xp + r0 * m.G * m.H, (int)nr,
+                         m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err, TB * m.I);
+        if (rc) return rc;
+      }
+    }
+  } else {
+    rc = split_planes(x, xpl, TB, m.I, s, g_err);
+    if (rc) return rc;
+  }
   for (int l = 0; l < m.L; ++l) {
     const int Il = m.in_size(l);
     TcRecurArgs a{};
@@ -232,8 +318,10 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
       whh[d] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
       float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
-      rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
-      if (rc) return rc;
+      if (!(chunked_in && l == 0)) {
+        rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
+        if (rc) return rc;
+      }
       a.xproj[d] = xp;
       a.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
       a.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
@@ -252,8 +340,56 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
     HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
     HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
+    const bool drain = last && ov && ov->y_host;
+    if (drain) {
+      a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);
+      HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
+      if ((rc = join(s, ov->cs))) return rc;  // counters zeroed before the copy stream polls them
+    }
+    static const bool dbg = getenv("HS_DEBUG_HOSTIO") != nullptr;
+    cudaEvent_t dbg_ev[12];
+    if (drain && dbg) {
+      for (int i = 0; i < 12; ++i) HS_CUDA(cudaEventCreate(&dbg_ev[i]));
+      HS_CUDA(cudaEventRecord(dbg_ev[0], s));
+    }
     rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
     if (rc) return rc;
+    if (drain && dbg) HS_CUDA(cudaEventRecord(dbg_ev[1], s));
+    if (drain) {
+      // y chunk [t0, t1) is final once every CTA has finished step s_need
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
+      WaitValue32Fn wait = wait_value_fn();
+      if (!wait && (rc = join(s, ov->cs))) return rc;  // no stream memory ops: drain after the kernel
+      const int nco = m.T < 16 ? m.T : 16;
+      const size_t row = (size_t)m.B * m.D * m.H;
+      for (int k = 0; k < nco; ++k) {
+        int t0, t1;
+        chunk_bounds(m.T, nco, k, &t0, &t1);
+        const int s_need = m.D == 1 ? t1 - 1 : (t1 - 1 > m.T - 1 - t0 ? t1 - 1 : m.T - 1 - t0);
+        if (wait) {
+          CUresult r = wait(ov->cs, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
+          if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        }
+        if (dbg && k < 8) HS_CUDA(cudaEventRecord(dbg_ev[2 + k], ov->cs));
+        HS_CUDA(cudaMemcpyAsync(ov->y_host + (size_t)t0 * row, y + (size_t)t0 * row, (size_t)(t1 - t0) * row * sizeof(float),
+                                cudaMemcpyDeviceToHost, ov->cs));
+      }
+      if (dbg) {
+        HS_CUDA(cudaEventRecord(dbg_ev[10], ov->cs));
+        HS_CUDA(cudaEventSynchronize(dbg_ev[10]));
+        HS_CUDA(cudaEventSynchronize(dbg_ev[1]));
+        float ms;
+        cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[1]);
+        fprintf(stderr, "[hsrnn] last recurrence %.3f ms; copy-chunk starts:", ms);
+        for (int k = 0; k < nco && k < 8; ++k) {
+          cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[2 + k]);
+          fprintf(stderr, " %.3f", ms);
+        }
+        cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[10]);
+        fprintf(stderr, "; drained at %.3f ms\n", ms);
+        for (int i = 0; i < 12; ++i) cudaEventDestroy(dbg_ev[i]);
+      }
+    }
     if (a.trace) {
       static unsigned long long host[160 * kTraceSteps * 16];
       HS_CUDA(cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s));
@@ -276,8 +412,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
 
 int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout& pl, const void* packed,
                  const float* x, const float* h0, const float* c0, float* y, float* hn, float* cn,
-                 void* ws, const WsLayout& wl, cudaStream_t s, float* layer_ms) {
-  if (algo == HS_ALGO_TC) return tc_forward(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, layer_ms);
+                 void* ws, const WsLayout& wl, cudaStream_t s, float* layer_ms, const Overlap* ov = nullptr) {
+  if (algo == HS_ALGO_TC) return tc_forward(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, layer_ms, ov);
   const size_t DBH = (size_t)m.D * m.B * m.H;
   float* zeros = at<float>(ws, wl.zeros);
   if (!h0 || (m.G == 4 && !c0)) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
@@ -422,6 +558,61 @@ int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed, const voi
   return forward_impl(m, algo, di, pl, packed, static_cast<const float*>(x), static_cast<const float*>(h0),
                       static_cast<const float*>(c0), static_cast<float*>(y), static_cast<float*>(hn),
                       static_cast<float*>(cn), workspace, wl, static_cast<cudaStream_t>(stream), layer_ms);
+}
+
+int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void* x_host, const void* h0_host,
+                        const void* c0_host, void* y_host, void* hn_host, void* cn_host, void* x_dev, void* y_dev,
+                        void* hn_dev, void* cn_dev, void* state_dev, void* workspace, size_t ws_bytes, void* stream) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!packed || !x_host || !y_host || !hn_host || !x_dev || !y_dev || !hn_dev || !workspace)
+    return fail(HS_ERR_INVALID, "packed, x/y/hn host and device buffers and workspace must be non-NULL");
+  if (m.G == 4 && (!cn_host || !cn_dev)) return fail(HS_ERR_INVALID, "LSTM needs c_n host and device buffers");
+  if ((h0_host || c0_host) && !state_dev) return fail(HS_ERR_INVALID, "initial states need a state_dev staging buffer");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  WsLayout wl = ws_layout(m);
+  if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t sbytes = sizeof(float) * (size_t)m.L * m.D * m.B * m.H;
+  float* h0d = nullptr;
+  float* c0d = nullptr;
+  if (h0_host) {
+    h0d = static_cast<float*>(state_dev);
+    HS_CUDA(cudaMemcpyAsync(h0d, h0_host, sbytes, cudaMemcpyHostToDevice, s));
+  }
+  if (c0_host && m.G == 4) {
+    c0d = static_cast<float*>(state_dev) + (size_t)m.L * m.D * m.B * m.H;
+    HS_CUDA(cudaMemcpyAsync(c0d, c0_host, sbytes, cudaMemcpyHostToDevice, s));
+  }
+  const size_t xbytes = sizeof(float) * (size_t)m.T * m.B * m.I;
+  const size_t ybytes = sizeof(float) * (size_t)m.T * m.B * m.D * m.H;
+  float* xd = static_cast<float*>(x_dev);
+  float* yd = static_cast<float*>(y_dev);
+  float* hnd = static_cast<float*>(hn_dev);
+  float* cnd = static_cast<float*>(cn_dev);
+  if (algo == HS_ALGO_TC) {
+    Overlap ov;
+    ov.x_host = static_cast<const float*>(x_host);
+    ov.y_host = static_cast<float*>(y_host);
+    if ((rc = copy_stream(&ov.cs))) return rc;
+    rc = forward_impl(m, algo, di, pl, packed, xd, h0d, c0d, yd, hnd, cnd, workspace, wl, s, nullptr, &ov);
+    if (rc) return rc;
+    if ((rc = join(ov.cs, s))) return rc;  // y drained before the call's work on s completes
+  } else {
+    HS_CUDA(cudaMemcpyAsync(xd, x_host, xbytes, cudaMemcpyHostToDevice, s));
+    rc = forward_impl(m, algo, di, pl, packed, xd, h0d, c0d, yd, hnd, cnd, workspace, wl, s, nullptr);
+    if (rc) return rc;
+    HS_CUDA(cudaMemcpyAsync(y_host, yd, ybytes, cudaMemcpyDeviceToHost, s));
+  }
+  HS_CUDA(cudaMemcpyAsync(hn_host, hnd, sbytes, cudaMemcpyDeviceToHost, s));
+  if (m.G == 4) HS_CUDA(cudaMemcpyAsync(cn_host, cnd, sbytes, cudaMemcpyDeviceToHost, s));
+  return HS_OK;
 }
 
 int hs_rnn_forward(const hs_rnn_desc* desc, const void* x, const void* const* w_ih, const void* const* w_hh,

@@ -128,9 +128,10 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// fp32 [rows, cols] (row stride ld) -> bf16 planes [2][rows][cols]
+// fp32 [rows, cols] (row stride ld) -> bf16 planes [2][rows][cols]; the lo
+// plane starts `pstride` elements after the hi plane (pstride = 0: rows*cols)
 __global__ void split_planes_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, size_t rows, int cols,
-                                    int ld) {
+                                    int ld, size_t pstride) {
   const size_t total = rows * (size_t)cols;
   for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; i < total; i += (size_t)gridDim.x * blockDim.x * 4) {
     const size_t r = i / cols;
@@ -141,7 +142,7 @@ __global__ void split_planes_kernel(const float* __restrict__ x, __nv_bfloat16* 
 #pragma unroll
     for (int j = 0; j < 4; ++j) ptx::split_bf16(f[j], hi[j], lo[j]);
     *reinterpret_cast<uint2*>(out + i) = *reinterpret_cast<uint2*>(hi);
-    *reinterpret_cast<uint2*>(out + total + i) = *reinterpret_cast<uint2*>(lo);
+    *reinterpret_cast<uint2*>(out + (pstride ? pstride : total) + i) = *reinterpret_cast<uint2*>(lo);
   }
 }
 

@@ -60,7 +60,7 @@ inline size_t packed_bytes(int G, int H, int I) {
 }
 
 struct TcWs {
-  size_t xpl, hbuf, counters, trace, total;
+  size_t xpl, hbuf, counters, trace, progress, total;
 };
 inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   (void)G;
@@ -71,6 +71,7 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   w.hbuf = off;     off += ((3 * (size_t)D * 2 * pad16(B) * H * 2) + 255) / 256 * 256;
   w.counters = off; off += 128 * 128;  // <= 128 chunk counters, one 128-B line each
   w.trace = off;    off += (size_t)160 * kTraceSteps * 16 * 8;
+  w.progress = off; off += ((size_t)T * 4 + 255) / 256 * 256;  // per-step output counters (host-buffer forward)
   w.total = off;
   return w;
 }
@@ -133,16 +134,17 @@ inline EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3D bf16 map {inner, rows, planes}, 128B swizzle, box {64, box_rows, 1}.
+// 3D bf16 map {inner, rows, planes}, 128B swizzle, box {64, box_rows, 1};
+// planes are `pstride` elements apart (0: inner*rows, i.e. dense).
 inline int make_map3(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t planes, uint32_t box_rows,
-                     std::string& err) {
+                     std::string& err, uint64_t pstride = 0) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     err = "cuTensorMapEncodeTiled unavailable";
     return 2;
   }
   cuuint64_t dims[3] = {inner, rows, planes};
-  cuuint64_t strides[2] = {inner * 2, inner * rows * 2};
+  cuuint64_t strides[2] = {inner * 2, (pstride ? pstride : inner * rows) * 2};
   cuuint32_t box[3] = {64, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -166,11 +168,12 @@ inline int set_smem(K kernel, size_t bytes, std::string& err) {
 }
 
 // K1 on planes: A planes [2][M][K], W_ih planes [2][N][K]
+// (a_pstride: element distance between the A hi and lo planes; 0 = M*K)
 inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const float* bias, float* C, int M, int N, int K,
-                       int npass, cudaStream_t s, std::string& err) {
+                       int npass, cudaStream_t s, std::string& err, size_t a_pstride = 0) {
   CUtensorMap ta, tb;
   const int BN = gemm_bn(N);
-  int rc = make_map3(&ta, apl, K, M, 2, GBM, err);
+  int rc = make_map3(&ta, apl, K, M, 2, GBM, err, a_pstride);
   if (!rc) rc = make_map3(&tb, wpl, K, N, 2, BN, err);
   if (rc) return rc;
   dim3 grid(N / BN, (M + GBM - 1) / GBM);
@@ -192,12 +195,13 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   return 0;
 }
 
-inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int cols, cudaStream_t s, std::string& err) {
+inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int cols, cudaStream_t s, std::string& err,
+                        size_t pstride = 0) {
   const size_t total = rows * cols;
   int blocks = (int)((total / 4 + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  split_planes_kernel<<<blocks, 256, 0, s>>>(x, out, rows, cols, cols);
+  split_planes_kernel<<<blocks, 256, 0, s>>>(x, out, rows, cols, cols, pstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("split_planes_kernel: ") + cudaGetErrorString(e);

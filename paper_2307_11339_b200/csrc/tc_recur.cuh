@@ -43,6 +43,7 @@ struct TcRecurArgs {
   __nv_bfloat16* hbuf;          // [3][D][NPL][Npad][H] bf16
   unsigned int* counters;       // [D][S]
   unsigned long long* trace;    // optional [grid][kTraceSteps][16] %globaltimer stamps (debug)
+  unsigned int* progress;       // optional [T]: progress[s] counts CTAs whose outputs of step s are in memory
 };
 
 constexpr int kTraceSteps = 64;
@@ -331,6 +332,10 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
     __syncthreads();  // all h_t stores of this CTA issued
     if (e == 128) HS_TRACE(8);
     if (e == 0 && !last) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
+    // the barrier above also ordered every thread's y stores of step s-1:
+    // publish them for the overlapped device->host copy (off the critical path)
+    if (a.progress && e == kEpiThreads - 32 && s > 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s - 1) : "memory");
     if (e == 0) HS_TRACE(10);
     // 3. off the critical path: layer outputs, final state, next step's XP
 #pragma unroll
@@ -357,6 +362,8 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   cluster_wait();
   ptx::tc_fence_before();
   __syncthreads();
+  if (a.progress && e == kEpiThreads - 32)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + T - 1) : "memory");
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, tcols);

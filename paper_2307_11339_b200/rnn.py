@@ -48,6 +48,7 @@ ABI_SYMBOLS = (
     "hs_rnn_pack_weights",
     "hs_rnn_forward_packed",
     "hs_rnn_forward",
+    "hs_rnn_forward_host",
     "hs_rnn_run_cells",
 )
 
@@ -171,6 +172,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_pack_weights.argtypes = [pd, pvp, pvp, pvp, pvp, vp, sz, vp]
     lib.hs_rnn_forward_packed.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, ctypes.POINTER(ctypes.c_float)]
     lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ABI_SYMBOLS[2:]:
         getattr(lib, name).restype = ctypes.c_int
@@ -305,6 +307,47 @@ class RNNExecutor:
         if layer_ms:
             return y, hn, cn, [[times[2 * l], times[2 * l + 1]] for l in range(s.layers)]
         return y, hn, cn
+
+    def alloc_host_outputs(self):
+        """Pinned host output buffers (y, h_n, c_n) for :meth:`forward_host`."""
+        return tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() if t is not None else None
+                     for t in self.alloc_outputs())
+
+    def forward_host(self, x_host: torch.Tensor, h0=None, c0=None, out_host=None, staging=None):
+        """End-to-end forward on host tensors (``hs_rnn_forward_host``): the
+        H2D upload of ``x`` and the D2H download of ``y`` overlap the compute
+        on the tensor-core path.  Host tensors should be pinned.  Returns the
+        host ``(y, h_n, c_n)``; work is complete when the current stream is."""
+        s = self.spec
+        for name, t in (("x", x_host), ("h0", h0), ("c0", c0)):
+            if t is not None and (t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous float32 host tensor")
+        if tuple(x_host.shape) != (s.seq, s.batch, s.I):
+            raise ValueError(f"x has shape {tuple(x_host.shape)}, expected {(s.seq, s.batch, s.I)}")
+        y, hn, cn = out_host if out_host is not None else self.alloc_host_outputs()
+        if staging is None:
+            staging = self.alloc_staging()
+        xd, (yd, hnd, cnd), state = staging
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            _check(
+                self.lib,
+                "hs_rnn_forward_host",
+                self.lib.hs_rnn_forward_host(
+                    ctypes.byref(self.desc), self.packed.data_ptr(), x_host.data_ptr(), ptr(h0), ptr(c0),
+                    y.data_ptr(), hn.data_ptr(), ptr(cn), xd.data_ptr(), yd.data_ptr(), hnd.data_ptr(), ptr(cnd),
+                    state.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), stream.cuda_stream,
+                ),
+            )
+        return y, hn, cn
+
+    def alloc_staging(self):
+        """Device staging buffers for :meth:`forward_host`: (x, (y, h_n, c_n), states)."""
+        s = self.spec
+        xd = torch.empty((s.seq, s.batch, s.I), device=self.device)
+        state = torch.empty((2, s.layers * s.dirs, s.batch, s.hidden), device=self.device)
+        return xd, self.alloc_outputs(), state
 
     def run_cells(self, ld: int, t0: int, t1: int, inp, out, h_prev, c_prev, h_last, c_last):
         """Steps ``t0..t1-1`` (processing order) of layer-direction ``ld``."""

@@ -39,17 +39,17 @@ class InferenceResponse:
 
 
 class RNNServer:
-    """Serves requests for one resident model with preallocated device input
-    and pinned host output buffers (no allocation on the request path)."""
+    """Serves requests for one resident model with preallocated device
+    staging and pinned host output buffers (no allocation on the request
+    path).  Host requests go through ``hs_rnn_forward_host``, which overlaps
+    the H2D upload of x and the D2H download of y with the compute."""
 
     def __init__(self, executor: RNNExecutor):
         self.ex = executor
         s = executor.spec
-        dev = executor.device
-        self.x_dev = torch.empty((s.seq, s.batch, s.I), device=dev)
-        self.state_dev = [torch.empty((s.layers * s.dirs, s.batch, s.hidden), device=dev) for _ in range(2)]
-        self.outs = executor.alloc_outputs()
-        self.host_outs = [torch.empty(t.shape, dtype=t.dtype).pin_memory() if t is not None else None for t in self.outs]
+        self.staging = executor.alloc_staging()
+        self.outs = self.staging[1]
+        self.host_outs = executor.alloc_host_outputs()
         self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 
     def run(self, req: InferenceRequest) -> InferenceResponse:
@@ -58,24 +58,22 @@ class RNNServer:
         if tuple(req.x.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"request x has shape {tuple(req.x.shape)}, model expects {(s.seq, s.batch, s.I)}")
         stream = torch.cuda.current_stream(ex.device)
+        on_host = req.x.device.type == "cpu"
         h2d = 0
         self.ev[0].record(stream)
-        self.x_dev.copy_(req.x, non_blocking=True)
-        h2d += req.x.numel() * req.x.element_size() if req.x.device.type == "cpu" else 0
-        states = []
-        for i, st in enumerate((req.h0, req.c0)):
-            if st is None:
-                states.append(None)
-                continue
-            self.state_dev[i].copy_(st, non_blocking=True)
-            h2d += st.numel() * st.element_size() if st.device.type == "cpu" else 0
-            states.append(self.state_dev[i])
-        ex.forward(self.x_dev, states[0], states[1], out=self.outs)
-        d2h = 0
-        for dst, src in zip(self.host_outs, self.outs):
-            if src is not None:
-                dst.copy_(src, non_blocking=True)
-                d2h += src.numel() * src.element_size()
+        if on_host:
+            h0 = req.h0.contiguous() if req.h0 is not None else None
+            c0 = req.c0.contiguous() if req.c0 is not None else None
+            ex.forward_host(req.x.contiguous(), h0, c0, out_host=self.host_outs, staging=self.staging)
+            h2d = sum(t.numel() * t.element_size() for t in (req.x, h0, c0) if t is not None)
+        else:
+            dev = ex.device
+            ex.forward(req.x, None if req.h0 is None else req.h0.to(dev), None if req.c0 is None else req.c0.to(dev),
+                       out=self.outs)
+            for dst, src in zip(self.host_outs, self.outs):
+                if src is not None:
+                    dst.copy_(src, non_blocking=True)
+        d2h = sum(t.numel() * t.element_size() for t in self.outs if t is not None)
         self.ev[1].record(stream)
         self.ev[1].synchronize()
         y, hn, cn = self.host_outs
