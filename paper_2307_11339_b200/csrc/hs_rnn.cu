@@ -324,6 +324,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       }
       a.xproj[d] = xp;
       a.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+      a.whh_scale[d] = whh_scales(at<unsigned char>(const_cast<void*>(packed), lp.tc), m.G, m.H, Il);
       a.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
       a.c0[d] = c0 ? c0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
       a.hn[d] = hn + (size_t)ld * m.B * m.H;
@@ -333,7 +334,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     const bool last = l == m.L - 1;
     a.y = last ? y : nullptr;
     a.ypl = last ? nullptr : xpl;
-    a.hbuf = hbuf;
+    a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
     static const char* trace_path = getenv("HS_RECUR_TRACE");
     a.trace = trace_path && l == 0 ? reinterpret_cast<unsigned long long*>(tcws + tw.trace) : nullptr;
@@ -532,7 +533,7 @@ int hs_rnn_pack_weights(const hs_rnn_desc* desc, const void* const* w_ih, const 
       HS_CUDA(cudaGetLastError());
       if (lp.tc) {
         rc = hs::tc::pack_layer(m.G, m.H, m.in_size(l), static_cast<const float*>(w_ih[ld]), static_cast<const float*>(w_hh[ld]),
-                                at<unsigned char>(packed, lp.tc), s, g_err);
+                                at<unsigned char>(packed, lp.tc), m.dtype != HS_DTYPE_BF16, s, g_err);
         if (rc) return rc;
       }
     }

@@ -54,9 +54,19 @@ inline int gemm_bn(int N) { return N % 256 == 0 ? 256 : 128; }
 // packed planes per layer-direction: W_ih [2][G*H][I] bf16, W_hh row-block packed [2][H/32*128][H] bf16
 inline size_t wih_plane_elems(int G, int H, int I) { return (size_t)G * H * I; }
 inline size_t whh_plane_elems(int H) { return (size_t)(H / 32) * 128 * H; }
+// + per-row power-of-two scales of the fp16 W_hh planes ([H/32*128] f32)
 inline size_t packed_bytes(int G, int H, int I) {
   if (H % 32) return 0;
-  return 2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H));
+  return 2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)) + 4 * (size_t)(H / 32) * 128;
+}
+
+inline float* whh_scales(void* packed_layer, int G, int H, int I) {
+  return reinterpret_cast<float*>(static_cast<unsigned char*>(packed_layer) +
+                                  2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)));
+}
+
+__global__ void fill_ones_kernel(float* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 1.f;
 }
 
 struct TcWs {
@@ -80,9 +90,40 @@ inline size_t workspace_bytes(int G, int H, int B, int T, int D, int I0) {
   return tc_ws_layout(G, H, B, T, D, I0).total;
 }
 
+// Per packed W_hh row: the power-of-two exponent e that brings the row's
+// max |w| to ~2^14 before the fp16 split, so W_lo = fp16(w*2^e - W_hi) stays
+// a normal fp16 (the tensor cores flush fp16 subnormals: unscaled, W_lo of
+// |w| ~ 1/32 weights would vanish).  Stores 2^-e, which the recurrent
+// epilogue applies to the gate pre-activation.  One warp per row.
+__global__ void whh_row_scale_kernel(const float* __restrict__ w_hh, float* __restrict__ inv_scale, int G, int H) {
+  const int rows = (H / 32) * 128;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int rb = r / 128, g = (r % 128) / 32, u = r % 32;
+    float m = 0.f;
+    if (g < G)
+      for (int k = lane; k < H; k += 32) m = fmaxf(m, fabsf(w_hh[((size_t)g * H + rb * 32 + u) * H + k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      int e = 0;
+      if (m > 0.f) {
+        int ex;
+        frexpf(m, &ex);  // m in [2^(ex-1), 2^ex)
+        e = 14 - ex;
+        e = e > 60 ? 60 : e < -60 ? -60 : e;
+      }
+      inv_scale[r] = ldexpf(1.f, -e);
+    }
+  }
+}
+
+// W_ih: bf16 hi/lo planes (K1 GEMM).  W_hh: fp16 hi/lo planes of the row-
+// scaled weights (f32 mode, whh_f16) or bf16 (bf16 mode uses plane 0 only),
+// row-block packed.
 __global__ void pack_tc_kernel(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
                                __nv_bfloat16* __restrict__ wih_pl, __nv_bfloat16* __restrict__ whh_pl, int G, int H,
-                               int I) {
+                               int I, int whh_f16, const float* __restrict__ inv_scale) {
   const size_t n_ih = (size_t)G * H * I;
   const size_t n_hh = (size_t)(H / 32) * 128 * H;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -97,18 +138,31 @@ __global__ void pack_tc_kernel(const float* __restrict__ w_ih, const float* __re
     const size_t r = i / H;
     const int rb = (int)(r / 128), g = (int)((r % 128) / 32), u = (int)(r % 32);
     const float v = g < G ? w_hh[((size_t)g * H + rb * 32 + u) * H + k] : 0.f;
-    __nv_bfloat16 hi, lo;
-    ptx::split_bf16(v, hi, lo);
-    whh_pl[i] = hi;
-    whh_pl[n_hh + i] = lo;
+    if (whh_f16) {
+      const float vs = v / inv_scale[r];  // exact: power of two
+      const __half hi = __float2half_rn(vs);
+      const __half lo = __float2half_rn(vs - __half2float(hi));
+      reinterpret_cast<uint16_t*>(whh_pl)[i] = __half_as_ushort(hi);
+      reinterpret_cast<uint16_t*>(whh_pl)[n_hh + i] = __half_as_ushort(lo);
+    } else {
+      __nv_bfloat16 hi, lo;
+      ptx::split_bf16(v, hi, lo);
+      whh_pl[i] = hi;
+      whh_pl[n_hh + i] = lo;
+    }
   }
 }
 
-inline int pack_layer(int G, int H, int I, const float* w_ih, const float* w_hh, unsigned char* dst, cudaStream_t s,
-                      std::string& err) {
+inline int pack_layer(int G, int H, int I, const float* w_ih, const float* w_hh, unsigned char* dst, bool whh_f16,
+                      cudaStream_t s, std::string& err) {
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(dst);
   __nv_bfloat16* whh = wih + 2 * wih_plane_elems(G, H, I);
-  pack_tc_kernel<<<592, 256, 0, s>>>(w_ih, w_hh, wih, whh, G, H, I);
+  float* inv_scale = whh_scales(dst, G, H, I);
+  whh_row_scale_kernel<<<148, 256, 0, s>>>(w_hh, inv_scale, G, H);
+  if (!whh_f16) {  // bf16 mode: unscaled
+    fill_ones_kernel<<<16, 256, 0, s>>>(inv_scale, (H / 32) * 128);
+  }
+  pack_tc_kernel<<<592, 256, 0, s>>>(w_ih, w_hh, wih, whh, G, H, I, whh_f16 ? 1 : 0, inv_scale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("pack_tc_kernel: ") + cudaGetErrorString(e);
@@ -322,7 +376,7 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   CUtensorMap w0, w1, hm;
   int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
-  if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * NPL, a.Npad, err);
+  if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D, a.Npad, err);
   if (rc) return rc;
   const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL).total;
   int cells = 1;
