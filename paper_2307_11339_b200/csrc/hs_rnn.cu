@@ -141,7 +141,7 @@ int pack_layout(const Dims& m, PackLayout* p) {
 
 // ----------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t xproj, act0, act1, cst, zeros, barrier, tc, total;
+  size_t xproj, xproj2, act0, act1, cst, zeros, barrier, tc, total;
 };
 
 WsLayout ws_layout(const Dims& m) {
@@ -149,6 +149,9 @@ WsLayout ws_layout(const Dims& m) {
   size_t off = 0;
   const size_t TB = (size_t)m.T * m.B;
   w.xproj = off;   off = align_up(off + sizeof(float) * m.D * TB * m.G * m.H);
+  // second input-projection buffer: layer l+1's K1 runs while layer l's
+  // recurrence still reads its own (tensor-core path, L > 1)
+  w.xproj2 = off;  off = align_up(off + (m.L > 1 ? sizeof(float) * m.D * TB * m.G * m.H : 0));
   w.act0 = off;    off = align_up(off + (m.L > 1 ? sizeof(float) * TB * m.D * m.H : 0));
   w.act1 = off;    off = align_up(off + (m.L > 2 ? sizeof(float) * TB * m.D * m.H : 0));
   w.cst = off;     off = align_up(off + sizeof(float) * m.D * m.B * m.H);
@@ -224,6 +227,16 @@ WaitValue32Fn wait_value_fn() {
     if (getenv("HS_DEBUG")) fprintf(stderr, "[hsrnn] cuStreamWaitValue32 %s\n", fn ? "available" : "unavailable");
   }
   return fn;
+}
+
+int gemm_stream(cudaStream_t* out) {
+  static thread_local cudaStream_t cache[16] = {};
+  int dev;
+  HS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
+  if (!cache[dev]) HS_CUDA(cudaStreamCreateWithFlags(&cache[dev], cudaStreamNonBlocking));
+  *out = cache[dev];
+  return HS_OK;
 }
 
 int copy_stream(cudaStream_t* out) {
@@ -307,8 +320,19 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
   }
+  // Layer overlap: layer l+1's input projection (K1) runs on a second stream,
+  // one time chunk at a time, as soon as layer l's recurrence has published
+  // that chunk (per-step progress counters + cuStreamWaitValue32) — on the
+  // SMs the persistent recurrence leaves free — into the other xproj buffer.
+  static const char* ovl_env = getenv("HS_LAYER_OVERLAP");
+  const bool overlap = m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
+  cudaStream_t gs = nullptr;
+  if (overlap && (rc = gemm_stream(&gs))) return rc;
+  float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
   for (int l = 0; l < m.L; ++l) {
     const int Il = m.in_size(l);
+    float* xpl_l = xpb[overlap ? (l & 1) : 0];
+    if (overlap && l > 0 && (rc = join(gs, s))) return rc;  // layer l's K1 chunks done
     TcRecurArgs a{};
     a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D;
     const __nv_bfloat16* whh[2] = {nullptr, nullptr};
@@ -317,8 +341,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const LayerPack& lp = pl.ld[ld];
       const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
       whh[d] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
-      float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
-      if (!(chunked_in && l == 0)) {
+      float* xp = xpl_l + (size_t)d * TB * m.G * m.H;
+      if (!(chunked_in && l == 0) && !(overlap && l > 0)) {
         rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
         if (rc) return rc;
       }
@@ -342,10 +366,13 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
     HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
     const bool drain = last && ov && ov->y_host;
-    if (drain) {
+    const bool feed_next = overlap && !last;
+    if (drain || feed_next) {
       a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);
       HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
-      if ((rc = join(s, ov->cs))) return rc;  // counters zeroed before the copy stream polls them
+      // counters zeroed before the copy / K1 stream polls them
+      if (drain && (rc = join(s, ov->cs))) return rc;
+      if (feed_next && (rc = join(s, gs))) return rc;
     }
     static const bool dbg = getenv("HS_DEBUG_HOSTIO") != nullptr;
     cudaEvent_t dbg_ev[12];
@@ -356,6 +383,28 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
     if (rc) return rc;
     if (drain && dbg) HS_CUDA(cudaEventRecord(dbg_ev[1], s));
+    if (feed_next) {
+      // K1 of layer l+1, chunk k, once every CTA has finished step s_need
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
+      const int In = m.in_size(l + 1);
+      const int nk = m.T < 8 ? m.T : 8;
+      for (int k = 0; k < nk; ++k) {
+        int t0, t1;
+        chunk_bounds(m.T, nk, k, &t0, &t1);
+        const int s_need = m.D == 1 ? t1 - 1 : (t1 - 1 > m.T - 1 - t0 ? t1 - 1 : m.T - 1 - t0);
+        CUresult r = wait_value_fn()(gs, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
+        for (int d = 0; d < m.D; ++d) {
+          const LayerPack& lpn = pl.ld[(l + 1) * m.D + d];
+          const __nv_bfloat16* wihn = at<__nv_bfloat16>(packed, lpn.tc);
+          float* xpn = xpb[(l + 1) & 1] + (size_t)d * TB * m.G * m.H;
+          rc = gemm_planes(xpl + r0 * In, wihn, at<float>(packed, lpn.bias_x), xpn + r0 * m.G * m.H, (int)nr,
+                           m.G * m.H, In, NPL == 2 ? 3 : 1, gs, g_err, TB * In);
+          if (rc) return rc;
+        }
+      }
+    }
     if (drain) {
       // y chunk [t0, t1) is final once every CTA has finished step s_need
       const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
