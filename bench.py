@@ -111,6 +111,15 @@ def cpu_info():
             "torch_threads": torch.get_num_threads()}
 
 
+def spec_name(spec) -> str:
+    from paper_2307_11339_b200.rnn import CONFIGS
+
+    for k, v in CONFIGS.items():
+        if (v.cell, v.layers, v.hidden, v.seq, v.dirs) == (spec.cell, spec.layers, spec.hidden, spec.seq, spec.dirs):
+            return k
+    return "custom"
+
+
 def oracle_forward_sample(spec, weights, x):
     """One float64 oracle forward (the reference-arm / cpu_baseline unit)."""
     from oracle.rnn_ref import rnn_forward_ref
@@ -140,7 +149,7 @@ def time_cpu_baseline(spec, budget_s: float, sample_batch: int):
         times.append(time.perf_counter() - t0)
     p50 = statistics.median(times)
     return {"value": sample_batch / p50, "unit": UNIT, "p50_ms": p50 * 1e3, "reps": reps,
-            "sample": f"{CONFIG_NAME} forward on {sample_batch} of {spec.batch} sequences (full T={spec.seq}, L={spec.layers}), float64 numpy oracle, median of {reps}"}
+            "sample": f"{spec_name(spec)} forward on {sample_batch} of {spec.batch} sequences (full T={spec.seq}, L={spec.layers}), float64 numpy oracle, median of {reps}"}
 
 
 def torch_cpu_reference(spec, sample_batch, reps=3):
@@ -149,7 +158,8 @@ def torch_cpu_reference(spec, sample_batch, reps=3):
 
     from paper_2307_11339_b200 import init_weights, make_input
 
-    m = torch.nn.LSTM(spec.I, spec.hidden, spec.layers) if spec.cell == "lstm" else torch.nn.GRU(spec.I, spec.hidden, spec.layers)
+    cls = torch.nn.LSTM if spec.cell == "lstm" else torch.nn.GRU
+    m = cls(spec.I, spec.hidden, spec.layers, bidirectional=spec.dirs == 2)
     x = make_input(spec, 1)[:, :sample_batch].contiguous()
     with torch.no_grad():
         m(x)
@@ -196,6 +206,71 @@ def reference_planner():
         return None
 
 
+def describe(spec) -> str:
+    kind = ("bi" if spec.dirs == 2 else "") + spec.cell.upper()
+    return f"{spec.layers}-layer {kind} H{spec.hidden} T{spec.seq} B{spec.batch}/GPU {spec.dtype}"
+
+
+def run_pipeline(args, spec, world, rank, local, dev):
+    """Layer pipeline over `world` GPUs: rank g owns
+    a contiguous layer range, hands [chunk, B, H] outputs to rank g+1 over
+    NCCL point-to-point (NVLink).  One timed step = `inflight` requests
+    streamed through the pipeline (default: one per stage, so the pipeline
+    is full in steady state); value = sequences/s of the whole pipeline."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_11339_b200 import init_weights, make_input
+    from paper_2307_11339_b200.parallel import LayerPipeline
+    from paper_2307_11339_b200.rnn import RNNExecutor
+
+    inflight = args.inflight or max(world, 1)
+    weights = init_weights(spec, 0)
+    pipe = LayerPipeline(spec, weights, rank, world, args.chunk, lambda sp, w: RNNExecutor(sp, w, device=dev))
+    xs = [make_input(spec, 1 + r).pin_memory() for r in range(inflight)] if rank == 0 else [None] * inflight
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        pipe.run_many(xs)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clocks:
+        for i in range(args.steps):
+            evs[i][0].record()
+            pipe.run_many(xs)
+            evs[i][1].record()
+        torch.cuda.synchronize(dev)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    if rank == 0:
+        seqs = spec.batch * inflight * args.steps
+        line = {
+            "metric": METRIC, "value": seqs / (total / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / args.steps, "p50_ms": statistics.median(step_ms),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if spec.dtype == "f32" else "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {describe(spec)}, layer-pipelined", "mode": "pipeline",
+                       "stages": world, "stage0_layers": [pipe.l0, pipe.l1] if rank == 0 else None,
+                       "chunk": args.chunk, "requests_per_step": inflight, "algo": getattr(pipe.model, "algo", None),
+                       "parallelism": f"layer pipeline x{world} (NCCL P2P hand-off, no collective)"},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_reference(args, spec):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -219,7 +294,7 @@ def run_reference(args, spec):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "p50_ms": p50,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{CONFIG_NAME}: 2-layer LSTM H1024 T128, forward; reference-arm step = {sample_batch}-sequence sample",
+        "config": {"workload": f"{args.config}: {describe(spec)} forward; reference-arm step = {sample_batch}-sequence sample",
                    "batch_per_gpu": spec.batch, "sample_batch": sample_batch},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["affinity"], "kind": "port",
                          "sample": f"float64 numpy oracle (oracle/rnn_ref.py) cell DAG forward on {sample_batch} sequences, all host threads via BLAS",
@@ -245,6 +320,10 @@ def main(argv=None):
     ap.add_argument("--cpu-sample-batch", type=int, default=64)
     ap.add_argument("--ref-sample-batch", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["shard", "pipeline"], default="shard",
+                    help="shard: N independent request shards (weak scaling); pipeline: layers split over N GPUs")
+    ap.add_argument("--chunk", type=int, default=32, help="pipeline mode: timesteps per hand-off chunk")
+    ap.add_argument("--inflight", type=int, default=0, help="pipeline mode: requests per timed step (default N)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -267,6 +346,8 @@ def main(argv=None):
     else:
         torch.cuda.set_device(0)
     dev = torch.device(f"cuda:{local if world > 1 else 0}")
+    if args.mode == "pipeline":
+        return run_pipeline(args, spec, world, rank, local, dev)
 
     from paper_2307_11339_b200 import init_weights, make_input
     from paper_2307_11339_b200.rnn import RNNExecutor
@@ -347,13 +428,13 @@ def main(argv=None):
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         tdoc = json.loads(tfile.read_text())
-        traffic = tdoc.get(f"{CONFIG_NAME}:{ex.algo}:recurrent")
+        traffic = tdoc.get(f"{args.config}:{ex.algo}:recurrent")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": p90,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if spec.dtype == "f32" else "bf16", "data": "synthetic",
-        "config": {"workload": f"{CONFIG_NAME}: 2-layer LSTM H1024 T128 B64/GPU fp32 forward (layers x timesteps DAG)",
+        "config": {"workload": f"{args.config}: {describe(spec)} forward (layers x timesteps DAG)",
                    "batch_per_gpu": spec.batch, "global_batch": B_total, "algo": ex.algo,
                    "parallelism": f"request-sharded x{world} (no collective)", "l2": "flushed (256 MiB write) before each timed step"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",

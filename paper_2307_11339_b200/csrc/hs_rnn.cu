@@ -325,7 +325,12 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   // that chunk (per-step progress counters + cuStreamWaitValue32) — on the
   // SMs the persistent recurrence leaves free — into the other xproj buffer.
   static const char* ovl_env = getenv("HS_LAYER_OVERLAP");
-  const bool overlap = m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
+  // batches too large for one co-resident recurrence run as equal slices,
+  // one persistent launch each (no progress counters then)
+  const int Bs = batch_slice(m.G, m.H, m.B, m.D, NPL);
+  if (!Bs) return fail(HS_ERR_UNSUPPORTED, "no tensor-core recurrence plan for B=%d", m.B);
+  const int nsl = (m.B + Bs - 1) / Bs;
+  const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
   cudaStream_t gs = nullptr;
   if (overlap && (rc = gemm_stream(&gs))) return rc;
   float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
@@ -334,7 +339,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     float* xpl_l = xpb[overlap ? (l & 1) : 0];
     if (overlap && l > 0 && (rc = join(gs, s))) return rc;  // layer l's K1 chunks done
     TcRecurArgs a{};
-    a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D;
+    a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D; a.Bst = m.B;
     const __nv_bfloat16* whh[2] = {nullptr, nullptr};
     for (int d = 0; d < m.D; ++d) {
       const int ld = l * m.D + d;
@@ -380,8 +385,34 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       for (int i = 0; i < 12; ++i) HS_CUDA(cudaEventCreate(&dbg_ev[i]));
       HS_CUDA(cudaEventRecord(dbg_ev[0], s));
     }
-    rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
-    if (rc) return rc;
+    if (nsl == 1) {
+      rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
+      if (rc) return rc;
+    } else {
+      for (int j = 0; j < nsl; ++j) {
+        const int b0 = j * Bs, bn = m.B - b0 < Bs ? m.B - b0 : Bs;
+        TcRecurArgs sa = a;
+        sa.B = bn;
+        sa.Npad = pad16(bn);
+        for (int d = 0; d < m.D; ++d) {
+          sa.xproj[d] = a.xproj[d] + (size_t)b0 * m.G * m.H;
+          sa.h0[d] = a.h0[d] + (size_t)b0 * m.H;
+          sa.c0[d] = a.c0[d] + (size_t)b0 * m.H;
+          sa.hn[d] = a.hn[d] + (size_t)b0 * m.H;
+          sa.cn[d] = a.cn[d] ? a.cn[d] + (size_t)b0 * m.H : nullptr;
+        }
+        sa.y = a.y ? a.y + (size_t)b0 * m.D * m.H : nullptr;
+        sa.ypl = a.ypl ? a.ypl + (size_t)b0 * m.D * m.H : nullptr;
+        sa.progress = nullptr;
+        sa.trace = nullptr;
+        if (j) {
+          HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
+          HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
+        }
+        rc = recurrence_layer(m.G, NPL, whh, sa, di.sms, s, g_err);
+        if (rc) return rc;
+      }
+    }
     if (drain && dbg) HS_CUDA(cudaEventRecord(dbg_ev[1], s));
     if (feed_next) {
       // K1 of layer l+1, chunk k, once every CTA has finished step s_need
@@ -408,8 +439,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     if (drain) {
       // y chunk [t0, t1) is final once every CTA has finished step s_need
       const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
-      WaitValue32Fn wait = wait_value_fn();
-      if (!wait && (rc = join(s, ov->cs))) return rc;  // no stream memory ops: drain after the kernel
+      WaitValue32Fn wait = nsl == 1 ? wait_value_fn() : nullptr;
+      if (!wait && (rc = join(s, ov->cs))) return rc;  // no stream memory ops / sliced: drain after the kernel
       const int nco = m.T < 16 ? m.T : 16;
       const size_t row = (size_t)m.B * m.D * m.H;
       for (int k = 0; k < nco; ++k) {

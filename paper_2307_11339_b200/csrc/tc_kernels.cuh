@@ -42,9 +42,20 @@ inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
   return best;
 }
 
+// Batch slice of the recurrence: the largest equal split of B whose slice
+// has a feasible K-split (slices run one after another; 0 = infeasible).
+inline int batch_slice(int G, int H, int B, int D, int NPL) {
+  for (int n = 1; n <= B; ++n) {
+    const int Bs = (B + n - 1) / n;
+    if (Bs <= 256 && choose_split(G, H, Bs, D, NPL, static_cta_limit) > 0) return Bs;
+    if (Bs <= 16) break;
+  }
+  return 0;
+}
+
 inline bool supports(int G, int H, int B, int I0, int DH, int D = 1, int NPL = 2) {
-  if (I0 % 64 || DH % 64 || (G * H) % 128 || H % 64 || B > 256) return false;
-  return choose_split(G, H, B, D, NPL, static_cta_limit) > 0;
+  if (I0 % 64 || DH % 64 || (G * H) % 128 || H % 64) return false;
+  return batch_slice(G, H, B, D, NPL) > 0;
 }
 
 inline bool profitable(int G, int H, int B, int T) { return H >= 256 && B >= 4 && (long)T * B >= 128; }

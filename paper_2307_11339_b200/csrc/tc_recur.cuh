@@ -31,6 +31,7 @@ constexpr int RMAXCELLS = 32;  // owner cells per epilogue thread (template CELL
 
 struct TcRecurArgs {
   int H, B, Npad, T, D, S;
+  int Bst;                      // batch stride of xproj / y / ypl rows (>= B when the batch is sliced)
   int RB;                       // row blocks per direction = H / 32
   const float* xproj[2];        // per dir [T][B][G*H] f32 (includes b_ih (+ b_hh for LSTM))
   const float* bias_h[2];       // per dir [G*H] (GRU b_hh) or nullptr
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   }
   auto load_xproj = [&](int step) {
     const int tt = d == 0 ? step : T - 1 - step;
-    const float* __restrict__ xp = a.xproj[d] + (size_t)tt * B * GH + unit;
+    const float* __restrict__ xp = a.xproj[d] + (size_t)tt * a.Bst * GH + unit;
 #pragma unroll
     for (int k = 0; k < CELLS; ++k) {
       const int b = b0 + k * bstep;
@@ -352,13 +353,13 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
       const int b = b0 + k * bstep;
       if (b >= B) continue;
       const float hv = h_reg[k];
-      const size_t yidx = ((size_t)t * B + b) * D * H + (size_t)d * H + unit;
+      const size_t yidx = ((size_t)t * a.Bst + b) * D * H + (size_t)d * H + unit;
       if (a.y) a.y[yidx] = hv;
       if (a.ypl) {
         __nv_bfloat16 hi, lo;
         ptx::split_bf16(hv, hi, lo);
         a.ypl[yidx] = hi;
-        a.ypl[(size_t)T * B * D * H + yidx] = lo;
+        a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
       }
       if (last) {
         a.hn[d][(size_t)b * H + unit] = hv;

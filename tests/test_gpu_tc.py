@@ -54,3 +54,19 @@ def test_tc_bf16_mode():
     err = run(spec)
     print(f"bf16 max-abs {err:.3e}")
     assert err <= 1e-2
+
+
+def test_tc_batch_sliced_bf16():
+    """A batch too large for one co-resident recurrence (c5 width, B=200, bf16)
+    runs as equal batch slices and still matches the oracle (bf16 budget)."""
+    spec = RNNSpec("lstm", 2, 1024, 6, 200, dirs=2, dtype="bf16")
+    err = run(spec)
+    print(f"sliced bf16 max-abs {err:.3e}")
+    assert err <= 1e-2
+
+
+def test_tc_c5_width_sharded_batch():
+    """c5 as one rank of the 8-way request shard sees it: B=32, bf16."""
+    err = run(CONFIGS["c5"].with_(seq=12, batch=32))
+    print(f"c5 shard bf16 max-abs {err:.3e}")
+    assert err <= 1e-2
