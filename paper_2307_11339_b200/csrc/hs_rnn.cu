@@ -13,6 +13,7 @@
 #include <string>
 
 #include "../../include/hs_rnn.h"
+#include "cluster_small.cuh"
 #include "simt_kernels.cuh"
 #include "tc_kernels.cuh"
 
@@ -97,6 +98,7 @@ int device_info(DeviceInfo* info) {
 struct LayerPack {
   size_t wih, bias_x, bias_h, whh_simt;  // fp32 planes
   size_t tc;                             // tensor-core planes (hs::tc layout), 0 if absent
+  size_t whh;                            // plain fp32 W_hh [G*H][H] (small-shape cluster kernel), 0 if absent
 };
 struct PackLayout {
   LayerPack ld[64];
@@ -118,6 +120,24 @@ int resolve_algo(const Dims& m, int* algo) {
   return HS_OK;
 }
 
+// Cluster size for the small-shape kernel (cluster_small.cuh), 0 if the
+// layer does not fit: prefer 16 CTAs (non-portable size), then 8, then 4.
+int small_cluster(const Dims& m) {
+  if (m.B > 64 || m.H > 512) return 0;
+  const int imax = m.I > m.D * m.H ? m.I : m.D * m.H;
+  const int cands[3] = {16, 8, 4};  // more CTAs: shorter per-step matvec (measured c1: 1.75 / 2.1 / 3.7 us per step)
+  static const char* c_env = getenv("HS_SMALL_C");  // experiments: force the cluster size
+  if (c_env) {
+    const int C = atoi(c_env);
+    return (C >= 1 && m.H % C == 0 && hs::small_smem_bytes(m.G, m.H, imax, m.B, C) <= 200 * 1024) ? C : 0;
+  }
+  for (int C : cands) {
+    if (m.H % C) continue;
+    if (hs::small_smem_bytes(m.G, m.H, imax, m.B, C) <= 200 * 1024) return C;
+  }
+  return 0;
+}
+
 int pack_layout(const Dims& m, PackLayout* p) {
   if (m.L * m.D > 64) return fail(HS_ERR_UNSUPPORTED, "at most 64 layer-directions");
   size_t off = 0;
@@ -133,6 +153,8 @@ int pack_layout(const Dims& m, PackLayout* p) {
       const size_t tcb = hs::tc::packed_bytes(m.G, m.H, m.in_size(l));
       lp.tc = tcb ? off : 0;
       off = align_up(off + tcb);
+      lp.whh = small_cluster(m) ? off : 0;
+      if (lp.whh) off = align_up(off + sizeof(float) * (size_t)GH * m.H);
     }
   }
   p->total = off;
@@ -179,6 +201,40 @@ int launch_gemm_simt(const float* A, const float* Bw, const float* bias, float* 
   dim3 grid((N + 127) / 128, (M + 127) / 128);
   hs::sgemm_tn_bias<<<grid, 256, 0, s>>>(A, Bw, bias, C, M, N, K);
   HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+int launch_small(const Dims& m, const hs::SmallArgs& sa, cudaStream_t s) {
+  const size_t smem = hs::small_smem_bytes(m.G, m.H, sa.I, m.B, sa.C);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(m.D * sa.C);
+  cfg.blockDim = dim3(hs::kSmallThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = sa.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (m.G == 4) {
+    static bool init = false;
+    if (!init) {
+      HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      init = true;
+    }
+    HS_CUDA(cudaLaunchKernelEx(&cfg, hs::recur_cluster_small<4>, sa));
+  } else {
+    static bool init = false;
+    if (!init) {
+      HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      init = true;
+    }
+    HS_CUDA(cudaLaunchKernelEx(&cfg, hs::recur_cluster_small<3>, sa));
+  }
   return HS_OK;
 }
 
@@ -504,9 +560,34 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
   if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
   const size_t TB = (size_t)m.T * m.B;
   const float* in = x;
+  const int C = pl.ld[0].whh ? small_cluster(m) : 0;
   for (int l = 0; l < m.L; ++l) {
     float* out = (l == m.L - 1) ? y : at<float>(ws, (l & 1) ? wl.act1 : wl.act0);
     const int Il = m.in_size(l);
+    if (C) {  // whole layer in one cluster per direction (input projection fused)
+      hs::SmallArgs sa{};
+      sa.H = m.H; sa.I = Il; sa.B = m.B; sa.T = m.T; sa.D = m.D; sa.C = C;
+      sa.x = in;
+      sa.y = out;
+      for (int d = 0; d < m.D; ++d) {
+        const int ld = l * m.D + d;
+        const LayerPack& lp = pl.ld[ld];
+        sa.w_ih[d] = at<float>(packed, lp.wih);
+        sa.w_hh[d] = at<float>(packed, lp.whh);
+        sa.bias_x[d] = at<float>(packed, lp.bias_x);
+        sa.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+        sa.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+        sa.c0[d] = c0 ? c0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+        sa.hn[d] = hn + (size_t)ld * m.B * m.H;
+        sa.cn[d] = cn ? cn + (size_t)ld * m.B * m.H : at<float>(ws, wl.cst) + (size_t)d * m.B * m.H;
+      }
+      if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
+      int rc = launch_small(m, sa, s);
+      if (rc) return rc;
+      if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
+      in = out;
+      continue;
+    }
     hs::RecurArgs ra{};
     ra.H = m.H; ra.B = m.B; ra.T = m.T; ra.D = m.D;
     ra.dir_lo = 0; ra.ndir = m.D; ra.s0 = 0; ra.s1 = m.T;
@@ -605,6 +686,8 @@ int hs_rnn_pack_weights(const hs_rnn_desc* desc, const void* const* w_ih, const 
       if (!w_ih[ld] || !w_hh[ld]) return fail(HS_ERR_INVALID, "weights of layer-direction %d are NULL", ld);
       const LayerPack& lp = pl.ld[ld];
       HS_CUDA(cudaMemcpyAsync(at<float>(packed, lp.wih), w_ih[ld], sizeof(float) * (size_t)GH * m.in_size(l), cudaMemcpyDeviceToDevice, s));
+      if (lp.whh)
+        HS_CUDA(cudaMemcpyAsync(at<float>(packed, lp.whh), w_hh[ld], sizeof(float) * (size_t)GH * m.H, cudaMemcpyDeviceToDevice, s));
       bias_fold<<<(GH + 255) / 256, 256, 0, s>>>(b_ih ? static_cast<const float*>(b_ih[ld]) : nullptr,
                                                  b_hh ? static_cast<const float*>(b_hh[ld]) : nullptr,
                                                  at<float>(packed, lp.bias_x), at<float>(packed, lp.bias_h), GH, m.G == 4);
