@@ -82,6 +82,10 @@ int hs_abi_version(void);
 /* Thread-local description of the last failure in this thread. */
 const char* hs_last_error(void);
 
+/* Kernels launched by the last hs_rnn_forward_packed / hs_rnn_forward_host /
+ * hs_rnn_run_cells call on this thread (memsets and copies excluded). */
+int hs_rnn_last_launch_count(void);
+
 /* Which algorithm hs_rnn_forward_packed would run for this descriptor
  * (HS_ALGO_SIMT or HS_ALGO_TC) on the current device. */
 int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo);

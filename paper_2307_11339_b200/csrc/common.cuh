@@ -6,6 +6,10 @@
 
 namespace hs {
 
+// kernels launched by the current forward call on this host thread
+// (hs_rnn_last_launch_count; reset at the start of every forward entry point)
+inline thread_local int g_launch_count = 0;
+
 // Full-precision activations: the f32 mode is held to max-abs 1e-4 against
 // the float64 oracle, so no __expf / tanh.approx here.
 __device__ __forceinline__ float sigmoidf_(float v) { return 1.0f / (1.0f + expf(-v)); }

@@ -201,6 +201,7 @@ int launch_gemm_simt(const float* A, const float* Bw, const float* bias, float* 
   dim3 grid((N + 127) / 128, (M + 127) / 128);
   hs::sgemm_tn_bias<<<grid, 256, 0, s>>>(A, Bw, bias, C, M, N, K);
   HS_CUDA(cudaGetLastError());
+  ++hs::g_launch_count;
   return HS_OK;
 }
 
@@ -235,6 +236,7 @@ int launch_small(const Dims& m, const hs::SmallArgs& sa, cudaStream_t s) {
     }
     HS_CUDA(cudaLaunchKernelEx(&cfg, hs::recur_cluster_small<3>, sa));
   }
+  ++hs::g_launch_count;
   return HS_OK;
 }
 
@@ -253,6 +255,7 @@ int launch_recur_simt(const Dims& m, const DeviceInfo& di, hs::RecurArgs& ra, cu
   } else {
     HS_CUDA(cudaLaunchCooperativeKernel((const void*)hs::recur_simt<3>, dim3(grid), dim3(hs::RTHREADS), args, sizeof(hs::RecurSmem<3>), s));
   }
+  ++hs::g_launch_count;
   return HS_OK;
 }
 
@@ -631,6 +634,8 @@ extern "C" {
 
 int hs_abi_version(void) { return HS_RNN_ABI_VERSION; }
 
+int hs_rnn_last_launch_count(void) { return hs::g_launch_count; }
+
 const char* hs_last_error(void) { return g_err.c_str(); }
 
 int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo) {
@@ -706,6 +711,7 @@ int hs_rnn_pack_weights(const hs_rnn_desc* desc, const void* const* w_ih, const 
 
 int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed, const void* x, const void* h0, const void* c0,
                           void* y, void* hn, void* cn, void* workspace, size_t ws_bytes, void* stream, float* layer_ms) {
+  hs::g_launch_count = 0;
   Dims m;
   int rc = check_desc(desc, &m);
   if (rc) return rc;
@@ -727,6 +733,7 @@ int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed, const voi
 int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void* x_host, const void* h0_host,
                         const void* c0_host, void* y_host, void* hn_host, void* cn_host, void* x_dev, void* y_dev,
                         void* hn_dev, void* cn_dev, void* state_dev, void* workspace, size_t ws_bytes, void* stream) {
+  hs::g_launch_count = 0;
   Dims m;
   int rc = check_desc(desc, &m);
   if (rc) return rc;
@@ -798,6 +805,7 @@ int hs_rnn_forward(const hs_rnn_desc* desc, const void* x, const void* const* w_
 int hs_rnn_run_cells(const hs_rnn_desc* desc, const void* packed, int32_t ld, int32_t t0, int32_t t1, const void* in,
                      void* out, const void* h_prev, const void* c_prev, void* h_last, void* c_last, void* workspace,
                      size_t ws_bytes, void* stream) {
+  hs::g_launch_count = 0;
   Dims m;
   int rc = check_desc(desc, &m);
   if (rc) return rc;

@@ -257,6 +257,7 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
     err = std::string("gemm_xproj_kernel launch: ") + cudaGetErrorString(e);
     return 2;
   }
+  ++g_launch_count;
   return 0;
 }
 
@@ -272,6 +273,7 @@ inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int col
     err = std::string("split_planes_kernel: ") + cudaGetErrorString(e);
     return 2;
   }
+  ++g_launch_count;
   return 0;
 }
 
@@ -345,6 +347,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
     err = std::string("recur_tc_kernel launch: ") + cudaGetErrorString(e);
     return 2;
   }
+  ++g_launch_count;
   return 0;
 }
 

@@ -42,6 +42,7 @@ GATES = {"lstm": 4, "gru": 3}
 ABI_SYMBOLS = (
     "hs_abi_version",
     "hs_last_error",
+    "hs_rnn_last_launch_count",
     "hs_rnn_resolve_algo",
     "hs_rnn_workspace",
     "hs_rnn_packed_size",
@@ -166,6 +167,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     pvp = ctypes.POINTER(vp)
     lib.hs_abi_version.restype = ctypes.c_int
     lib.hs_last_error.restype = ctypes.c_char_p
+    lib.hs_rnn_last_launch_count.restype = ctypes.c_int
     lib.hs_rnn_resolve_algo.argtypes = [pd, ctypes.POINTER(i32)]
     lib.hs_rnn_workspace.argtypes = [pd, ctypes.POINTER(sz)]
     lib.hs_rnn_packed_size.argtypes = [pd, ctypes.POINTER(sz)]
@@ -174,7 +176,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
-    for name in ABI_SYMBOLS[2:]:
+    for name in ABI_SYMBOLS[3:]:
         getattr(lib, name).restype = ctypes.c_int
     if lib.hs_abi_version() != 1:
         raise RuntimeError(f"{lib_path}: ABI version {lib.hs_abi_version()} != 1")
@@ -267,12 +269,10 @@ class RNNExecutor:
                 ),
             )
 
-    def launches_per_forward(self) -> int:
-        """Kernels this library launches per forward (memsets excluded):
-        per layer one input-projection GEMM per direction plus one persistent
-        recurrent kernel covering both directions."""
-        s = self.spec
-        return s.layers * (s.dirs + 1)
+    def last_launch_count(self) -> int:
+        """Kernels the library launched in the last forward call on this
+        thread (``hs_rnn_last_launch_count``; memsets and copies excluded)."""
+        return int(self.lib.hs_rnn_last_launch_count())
 
     def alloc_outputs(self, batch: int | None = None):
         s = self.spec

@@ -140,3 +140,16 @@ def test_run_cells_segments_equal_whole():
         assert torch.equal(a_, b_)
     for a_, b_ in zip(whole, (y, hn, cn)):
         assert float((a_ - b_).abs().max()) <= 1e-6
+
+
+def test_launch_count_reports_library_kernels():
+    """hs_rnn_last_launch_count: the kernels of the last forward (the bench's
+    gpu_launches evidence) — tensor-core c2 and the small-shape cluster path."""
+    spec = CONFIGS["c2"].with_(seq=16)
+    ex = RNNExecutor(spec, init_weights(spec))
+    ex.forward(make_input(spec).to(ex.device))
+    # split + layer-0 K1 + 2 recurrences + layer-1 K1 (whole or 8 overlapped chunks)
+    assert ex.last_launch_count() in (5, 12)
+    small = RNNExecutor(CONFIGS["c1"], init_weights(CONFIGS["c1"]))
+    small.forward(make_input(CONFIGS["c1"]).to(small.device))
+    assert small.last_launch_count() == 1  # the whole layer in one cluster launch
