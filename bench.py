@@ -395,23 +395,23 @@ def main(argv=None):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = max_over_ranks(sum(step_ms))
 
-    # ---- end-to-end through the public request API (pinned host buffers)
+    # ---- end-to-end through the public request API (pinned host buffers):
+    # a stream of K requests through RNNServer.run_stream — every request's
+    # H2D of x and D2H of y/h_n/c_n inside the timed region; request i+1's
+    # upload overlaps request i's compute (two staging slots)
     server = RNNServer(ex)
     req = InferenceRequest(x=x_host)
-    for _ in range(2):
-        server.run(req)
-    e2e_ms = []
+    server.run_stream([req] * 2)
+    lat = [server.run(req).device_ms for _ in range(5)]  # single-request latency (sync)
     barrier()
     torch.cuda.synchronize(dev)
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)
-        resp = server.run(req)
-        e2e_ms.append(resp.device_ms)
+    summary = server.run_stream([req] * args.steps)
     torch.cuda.synchronize(dev)
     barrier()
-    e2e_total = max_over_ranks(sum(e2e_ms))
-    h2d = resp.h2d_bytes
-    d2h = resp.d2h_bytes
+    e2e_total = max_over_ranks(summary.device_ms)
+    h2d = summary.h2d_bytes // args.steps
+    d2h = summary.d2h_bytes // args.steps
+    e2e_ms = lat
 
     if rank != 0:
         dist.destroy_process_group()
@@ -438,14 +438,17 @@ def main(argv=None):
         "dtype": "f32" if spec.dtype == "f32" else "bf16", "data": "synthetic",
         "config": {"workload": f"{args.config}: {describe(spec)} forward (layers x timesteps DAG)",
                    "batch_per_gpu": spec.batch, "global_batch": B_total, "algo": ex.algo,
-                   "parallelism": f"request-sharded x{world} (no collective)", "l2": "flushed (256 MiB write) before each timed step"},
+                   "parallelism": f"request-sharded x{world} (no collective)", "l2": "flushed (256 MiB write) before each timed step",
+                   "e2e_l2": "no flush; per-request working set (2 x 128 MiB xproj + 32 MiB x + 32 MiB y) exceeds the 126 MB L2"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
                      "kernel": f"recurrent wavefront ({ex.algo})", "kernel_ms_per_forward": rec_ms,
                      "gemm_ms_per_forward": gemm_ms, "algorithmic_flops": rec_f,
                      "peak_source": f"{peaks['source']} dense bf16 (burst)"},
         "e2e": {"value": B_total * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "p50_ms": statistics.median(e2e_ms)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
+                "single_request_p50_ms": statistics.median(e2e_ms),
+                "api": "RNNServer.run_stream (hs_rnn_forward_host), pinned host x in / y,h_n,c_n out every step"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

@@ -269,8 +269,29 @@ int launch_recur_simt(const Dims& m, const DeviceInfo& di, hs::RecurArgs& ra, cu
 struct Overlap {
   const float* x_host = nullptr;
   float* y_host = nullptr;
-  cudaStream_t cs = nullptr;
+  cudaStream_t cs_in = nullptr;   // x uploads (H2D)
+  cudaStream_t cs_out = nullptr;  // y downloads (D2H); separate so PCIe runs both directions at once
 };
+
+// Per x staging buffer: an event recorded once the forward has consumed it
+// (last split of x into bf16 planes).  The next upload into the same buffer
+// waits only for that — not for the whole previous forward — so a caller
+// alternating two staging buffers overlaps request k+1's upload with
+// request k's compute.
+int x_free_event(const void* x_dev, cudaEvent_t* ev, bool* seen) {
+  struct Entry { const void* p; cudaEvent_t ev; };
+  static thread_local Entry cache[8] = {};
+  static thread_local int next = 0;
+  for (auto& e : cache)
+    if (e.p == x_dev && e.ev) { *ev = e.ev; *seen = true; return HS_OK; }
+  Entry& e = cache[next];
+  next = (next + 1) % 8;
+  if (!e.ev) HS_CUDA(cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming));
+  e.p = x_dev;
+  *ev = e.ev;
+  *seen = false;
+  return HS_OK;
+}
 
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValue32Fn wait_value_fn() {
@@ -298,13 +319,13 @@ int gemm_stream(cudaStream_t* out) {
   return HS_OK;
 }
 
-int copy_stream(cudaStream_t* out) {
-  static thread_local cudaStream_t cache[16] = {};
+int copy_stream(int which, cudaStream_t* out) {
+  static thread_local cudaStream_t cache[2][16] = {};
   int dev;
   HS_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
-  if (!cache[dev]) HS_CUDA(cudaStreamCreateWithFlags(&cache[dev], cudaStreamNonBlocking));
-  *out = cache[dev];
+  if (!cache[which][dev]) HS_CUDA(cudaStreamCreateWithFlags(&cache[which][dev], cudaStreamNonBlocking));
+  *out = cache[which][dev];
   return HS_OK;
 }
 
@@ -349,16 +370,23 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   if (chunked_in) {
     // upload x in time chunks on the copy stream; split + layer-0 K1 per chunk
     const int nci = m.T < 16 ? m.T : 16;
-    if ((rc = join(s, ov->cs))) return rc;  // x staging is free once earlier work on s is done
+    cudaEvent_t x_free;
+    bool seen;
+    if ((rc = x_free_event(x, &x_free, &seen))) return rc;
+    if (seen) {
+      HS_CUDA(cudaStreamWaitEvent(ov->cs_in, x_free, 0));  // previous forward done reading this buffer
+    } else if ((rc = join(s, ov->cs_in))) {
+      return rc;
+    }
     cudaEvent_t ev_in[16];
     for (int k = 0; k < nci; ++k) {
       int t0, t1;
       chunk_bounds(m.T, nci, k, &t0, &t1);
       const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
       HS_CUDA(cudaMemcpyAsync(const_cast<float*>(x) + r0 * m.I, ov->x_host + r0 * m.I, nr * m.I * sizeof(float),
-                              cudaMemcpyHostToDevice, ov->cs));
+                              cudaMemcpyHostToDevice, ov->cs_in));
       HS_CUDA(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
-      HS_CUDA(cudaEventRecord(ev_in[k], ov->cs));
+      HS_CUDA(cudaEventRecord(ev_in[k], ov->cs_in));
     }
     for (int k = 0; k < nci; ++k) {
       int t0, t1;
@@ -375,6 +403,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         if (rc) return rc;
       }
     }
+    HS_CUDA(cudaEventRecord(x_free, s));  // x consumed: the next upload into it may start
   } else {
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
@@ -435,7 +464,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);
       HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
       // counters zeroed before the copy / K1 stream polls them
-      if (drain && (rc = join(s, ov->cs))) return rc;
+      if (drain && (rc = join(s, ov->cs_out))) return rc;
       if (feed_next && (rc = join(s, gs))) return rc;
     }
     static const bool dbg = getenv("HS_DEBUG_HOSTIO") != nullptr;
@@ -499,7 +528,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       // y chunk [t0, t1) is final once every CTA has finished step s_need
       const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
       WaitValue32Fn wait = nsl == 1 ? wait_value_fn() : nullptr;
-      if (!wait && (rc = join(s, ov->cs))) return rc;  // no stream memory ops / sliced: drain after the kernel
+      if (!wait && (rc = join(s, ov->cs_out))) return rc;  // no stream memory ops / sliced: drain after the kernel
       const int nco = m.T < 16 ? m.T : 16;
       const size_t row = (size_t)m.B * m.D * m.H;
       for (int k = 0; k < nco; ++k) {
@@ -507,15 +536,15 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         chunk_bounds(m.T, nco, k, &t0, &t1);
         const int s_need = m.D == 1 ? t1 - 1 : (t1 - 1 > m.T - 1 - t0 ? t1 - 1 : m.T - 1 - t0);
         if (wait) {
-          CUresult r = wait(ov->cs, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
+          CUresult r = wait(ov->cs_out, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
           if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
         }
-        if (dbg && k < 8) HS_CUDA(cudaEventRecord(dbg_ev[2 + k], ov->cs));
+        if (dbg && k < 8) HS_CUDA(cudaEventRecord(dbg_ev[2 + k], ov->cs_out));
         HS_CUDA(cudaMemcpyAsync(ov->y_host + (size_t)t0 * row, y + (size_t)t0 * row, (size_t)(t1 - t0) * row * sizeof(float),
-                                cudaMemcpyDeviceToHost, ov->cs));
+                                cudaMemcpyDeviceToHost, ov->cs_out));
       }
       if (dbg) {
-        HS_CUDA(cudaEventRecord(dbg_ev[10], ov->cs));
+        HS_CUDA(cudaEventRecord(dbg_ev[10], ov->cs_out));
         HS_CUDA(cudaEventSynchronize(dbg_ev[10]));
         HS_CUDA(cudaEventSynchronize(dbg_ev[1]));
         float ms;
@@ -771,10 +800,11 @@ int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void*
     Overlap ov;
     ov.x_host = static_cast<const float*>(x_host);
     ov.y_host = static_cast<float*>(y_host);
-    if ((rc = copy_stream(&ov.cs))) return rc;
+    if ((rc = copy_stream(0, &ov.cs_in))) return rc;
+    if ((rc = copy_stream(1, &ov.cs_out))) return rc;
     rc = forward_impl(m, algo, di, pl, packed, xd, h0d, c0d, yd, hnd, cnd, workspace, wl, s, nullptr, &ov);
     if (rc) return rc;
-    if ((rc = join(ov.cs, s))) return rc;  // y drained before the call's work on s completes
+    if ((rc = join(ov.cs_out, s))) return rc;  // y drained before the call's work on s completes
   } else {
     HS_CUDA(cudaMemcpyAsync(xd, x_host, xbytes, cudaMemcpyHostToDevice, s));
     rc = forward_impl(m, algo, di, pl, packed, xd, h0d, c0d, yd, hnd, cnd, workspace, wl, s, nullptr);

@@ -39,45 +39,109 @@ class InferenceResponse:
 
 
 class RNNServer:
-    """Serves requests for one resident model with preallocated device
-    staging and pinned host output buffers (no allocation on the request
-    path).  Host requests go through ``hs_rnn_forward_host``, which overlaps
-    the H2D upload of x and the D2H download of y with the compute."""
+    """Serves requests for one resident model.
 
-    def __init__(self, executor: RNNExecutor):
+    Device staging and pinned host outputs are preallocated in ``slots``
+    sets, so the request path allocates nothing.  Host requests go through
+    ``hs_rnn_forward_host``: within a request, the H2D upload of x and the
+    D2H download of y overlap the compute.  :meth:`run_stream` also overlaps
+    requests with each other: request i+1's upload runs during request i's
+    compute (alternating staging slots; the library makes an upload wait only
+    for the previous forward that used the same staging buffer).
+    """
+
+    def __init__(self, executor: RNNExecutor, slots: int = 2):
         self.ex = executor
-        s = executor.spec
-        self.staging = executor.alloc_staging()
-        self.outs = self.staging[1]
-        self.host_outs = executor.alloc_host_outputs()
+        self.slots = max(1, slots)
+        self.staging = [executor.alloc_staging() for _ in range(self.slots)]
+        self.host_outs = [executor.alloc_host_outputs() for _ in range(self.slots)]
+        self.outs = self.staging[0][1]
         self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self._next = 0
 
-    def run(self, req: InferenceRequest) -> InferenceResponse:
-        ex = self.ex
-        s = ex.spec
+    def _check(self, req: InferenceRequest):
+        s = self.ex.spec
         if tuple(req.x.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"request x has shape {tuple(req.x.shape)}, model expects {(s.seq, s.batch, s.I)}")
-        stream = torch.cuda.current_stream(ex.device)
-        on_host = req.x.device.type == "cpu"
-        h2d = 0
-        self.ev[0].record(stream)
-        if on_host:
+
+    def _submit(self, req: InferenceRequest, slot: int) -> tuple[int, int]:
+        """Enqueue one request on the current stream; returns (h2d, d2h) bytes."""
+        ex = self.ex
+        staging = self.staging[slot]
+        host_outs = self.host_outs[slot]
+        if req.x.device.type == "cpu":
             h0 = req.h0.contiguous() if req.h0 is not None else None
             c0 = req.c0.contiguous() if req.c0 is not None else None
-            ex.forward_host(req.x.contiguous(), h0, c0, out_host=self.host_outs, staging=self.staging)
+            ex.forward_host(req.x.contiguous(), h0, c0, out_host=host_outs, staging=staging)
             h2d = sum(t.numel() * t.element_size() for t in (req.x, h0, c0) if t is not None)
         else:
             dev = ex.device
+            outs = staging[1]
             ex.forward(req.x, None if req.h0 is None else req.h0.to(dev), None if req.c0 is None else req.c0.to(dev),
-                       out=self.outs)
-            for dst, src in zip(self.host_outs, self.outs):
+                       out=outs)
+            for dst, src in zip(host_outs, outs):
                 if src is not None:
                     dst.copy_(src, non_blocking=True)
-        d2h = sum(t.numel() * t.element_size() for t in self.outs if t is not None)
+            h2d = 0
+        d2h = sum(t.numel() * t.element_size() for t in staging[1] if t is not None)
+        return h2d, d2h
+
+    def run(self, req: InferenceRequest) -> InferenceResponse:
+        """One request, synchronously: returns host outputs and the device
+        time of H2D + forward + D2H (CUDA events)."""
+        self._check(req)
+        stream = torch.cuda.current_stream(self.ex.device)
+        slot = self._next
+        self._next = (self._next + 1) % self.slots
+        self.ev[0].record(stream)
+        h2d, d2h = self._submit(req, slot)
         self.ev[1].record(stream)
         self.ev[1].synchronize()
-        y, hn, cn = self.host_outs
+        y, hn, cn = self.host_outs[slot]
         return InferenceResponse(y, hn, cn, self.ev[0].elapsed_time(self.ev[1]), h2d, d2h)
+
+    def run_stream(self, requests, consume=None) -> InferenceResponse:
+        """Pipelined stream of requests (a serving loop).  ``consume(i, resp)``
+        is called once request i's outputs are on the host, before its slot
+        is reused.  Returns a summary response: the last request's outputs,
+        device_ms for the whole stream, and total H2D/D2H bytes."""
+        stream = torch.cuda.current_stream(self.ex.device)
+        done = [None] * self.slots
+        pending = [None] * self.slots
+        h2d_total = d2h_total = 0
+
+        def finish(slot):
+            done[slot].synchronize()
+            i, h2d, d2h = pending[slot]
+            y, hn, cn = self.host_outs[slot]
+            if consume is not None:
+                consume(i, InferenceResponse(y, hn, cn, float("nan"), h2d, d2h))
+            pending[slot] = None
+
+        self.ev[0].record(stream)
+        for i, req in enumerate(requests):
+            self._check(req)
+            slot = i % self.slots
+            if pending[slot] is not None:
+                finish(slot)
+            h2d, d2h = self._submit(req, slot)
+            h2d_total += h2d
+            d2h_total += d2h
+            ev = done[slot] or torch.cuda.Event()
+            ev.record(stream)
+            done[slot] = ev
+            pending[slot] = (i, h2d, d2h)
+        last = None
+        for k in range(self.slots):
+            slot = (len(requests) + k) % self.slots
+            if pending[slot] is not None:
+                last = slot
+                finish(slot)
+        self.ev[1].record(stream)
+        self.ev[1].synchronize()
+        y, hn, cn = self.host_outs[last if last is not None else 0]
+        return InferenceResponse(y, hn, cn, self.ev[0].elapsed_time(self.ev[1]), h2d_total, d2h_total,
+                                 extra={"requests": len(requests)})
 
 
 _SERVERS: dict[str, RNNServer] = {}

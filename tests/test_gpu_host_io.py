@@ -47,3 +47,21 @@ def test_run_request_host_path():
     y, hn, cn = ex.forward(x.to(ex.device))
     assert torch.equal(resp.y, y.cpu()) and torch.equal(resp.hn, hn.cpu()) and torch.equal(resp.cn, cn.cpu())
     assert resp.h2d_bytes == x.numel() * 4 and resp.device_ms > 0
+
+
+def test_run_stream_pipelined_requests():
+    """RNNServer.run_stream: request i+1's upload overlaps request i's compute
+    (alternating staging slots); every request's outputs must still be exact."""
+    from paper_2307_11339_b200 import RNNServer
+
+    spec = CONFIGS["c2"].with_(seq=24)
+    ex = RNNExecutor(spec, init_weights(spec, 4))
+    xs = [make_input(spec, 10 + i).pin_memory() for i in range(5)]
+    refs = [[t.cpu() for t in ex.forward(x.to(ex.device))] for x in xs]
+    server = RNNServer(ex)
+    got = {}
+    server.run_stream([InferenceRequest(x=x) for x in xs], consume=lambda i, r: got.__setitem__(i, (r.y.clone(), r.hn.clone(), r.cn.clone())))
+    assert sorted(got) == list(range(5))
+    for i in range(5):
+        for g, r in zip(got[i], refs[i]):
+            assert torch.equal(g, r)
