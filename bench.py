@@ -206,6 +206,27 @@ def reference_planner():
         return None
 
 
+def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic):
+    """Roofline of the dominant kernel, the recurrence.  W_hh resident on chip
+    (SMEM): bound by the tensor pipe — achieved = algorithmic recurrent FLOPs
+    / time vs the measured bf16 peak.  W_hh streamed every step (it does not
+    fit on chip, e.g. c4): bound by memory — algorithmic bytes per forward =
+    T*L*D*(W_hh at 4 B/weight + xproj row reads + y writes) vs measured HBM."""
+    common = {"kernel": f"recurrent wavefront ({algo})", "kernel_ms_per_forward": rec_ms,
+              "gemm_ms_per_forward": gemm_ms, "traffic": traffic}
+    if plan.get("w_ring"):
+        G, H, B, T = spec.G, spec.hidden, spec.batch, spec.seq
+        per_step = 4.0 * G * H * H + 4.0 * B * G * H + 4.0 * B * H
+        nbytes = T * spec.layers * spec.dirs * per_step
+        gbs = nbytes / (rec_ms / 1e3) / 1e9
+        return dict(common, bound="hbm", achieved=gbs, peak=peaks["hbm_gbs"], unit="GB/s", frac=gbs / peaks["hbm_gbs"],
+                    algorithmic_bytes=nbytes, peak_source=f"{peaks['source']} HBM copy")
+    tf = rec_f / (rec_ms / 1e3) / 1e12
+    return dict(common, bound="tensor", achieved=tf, peak=peaks["bf16_tflops"], unit="TFLOP/s",
+                frac=tf / peaks["bf16_tflops"], algorithmic_flops=rec_f,
+                peak_source=f"{peaks['source']} dense bf16 (burst)")
+
+
 def describe(spec) -> str:
     kind = ("bi" if spec.dirs == 2 else "") + spec.cell.upper()
     return f"{spec.layers}-layer {kind} H{spec.hidden} T{spec.seq} B{spec.batch}/GPU {spec.dtype}"
@@ -425,7 +446,7 @@ def main(argv=None):
     rec_ms = statistics.mean(sum(l[1] for l in lm) for lm in layer_ms)  # all layers, per forward
     gemm_ms = statistics.mean(sum(l[0] for l in lm) for lm in layer_ms)
     peaks = load_peaks()
-    achieved = rec_f / (rec_ms / 1e3) / 1e12
+    plan = ex.plan()
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
@@ -440,11 +461,8 @@ def main(argv=None):
                    "batch_per_gpu": spec.batch, "global_batch": B_total, "algo": ex.algo,
                    "parallelism": f"request-sharded x{world} (no collective)", "l2": "flushed (256 MiB write) before each timed step",
                    "e2e_l2": "no flush; per-request working set (2 x 128 MiB xproj + 32 MiB x + 32 MiB y) exceeds the 126 MB L2"},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                     "kernel": f"recurrent wavefront ({ex.algo})", "kernel_ms_per_forward": rec_ms,
-                     "gemm_ms_per_forward": gemm_ms, "algorithmic_flops": rec_f,
-                     "peak_source": f"{peaks['source']} dense bf16 (burst)"},
+        "roofline": roofline_entry(spec, plan, ex.algo, rec_f, rec_ms, gemm_ms, peaks, traffic),
+        "plan": plan,
         "e2e": {"value": B_total * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
                 "single_request_p50_ms": statistics.median(e2e_ms),

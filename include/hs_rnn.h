@@ -90,6 +90,13 @@ int hs_rnn_last_launch_count(void);
  * (HS_ALGO_SIMT or HS_ALGO_TC) on the current device. */
 int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo);
 
+/* Execution plan the library picks for this descriptor (static device
+ * limits), 8 ints: [0] algo (HS_ALGO_*), [1] tensor-core K-split cluster size
+ * S, or the small-shape kernel's cluster size C (SIMT), [2] W_hh ring depth
+ * (0 = W_hh resident in shared memory, > 0 = streamed from L2 every step),
+ * [3] batch slices, [4] 1 if the small-shape cluster kernel runs, [5..7] 0. */
+int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info);
+
 /* Bytes of device workspace needed by hs_rnn_forward_packed / run_cells. */
 int hs_rnn_workspace(const hs_rnn_desc* desc, size_t* bytes);
 

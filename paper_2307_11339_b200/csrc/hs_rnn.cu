@@ -679,6 +679,30 @@ int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo) {
   return HS_OK;
 }
 
+int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info) {
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!info) return fail(HS_ERR_INVALID, "info out-pointer is NULL");
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  info[0] = algo;
+  if (algo == HS_ALGO_TC) {
+    const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
+    const int Bs = hs::tc::batch_slice(m.G, m.H, m.B, m.D, NPL);
+    int nsw = 0;
+    info[1] = hs::tc::plan_split(m.G, m.H, Bs, m.D, NPL, hs::tc::static_cta_limit, &nsw);
+    info[2] = nsw;
+    info[3] = Bs ? (m.B + Bs - 1) / Bs : 0;
+  } else {
+    info[1] = small_cluster(m);
+    info[3] = 1;
+    info[4] = info[1] ? 1 : 0;
+  }
+  return HS_OK;
+}
+
 int hs_rnn_workspace(const hs_rnn_desc* desc, size_t* bytes) {
   Dims m;
   int rc = check_desc(desc, &m);

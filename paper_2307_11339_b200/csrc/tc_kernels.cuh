@@ -25,21 +25,38 @@ inline int pad16(int b) { return (b + 15) / 16 * 16; }
 // (cluster placement strands SMs: measured 15 clusters of 8 on a B200).
 inline int static_cta_limit(int S) { return S <= 2 ? 148 : S == 4 ? 132 : 120; }
 
+// W-streaming ring depth, used when the W_hh slices cannot stay resident
+// (e.g. c4, H = 2048: 64 MiB of fp16 hi/lo planes per layer-direction).
+constexpr int kSW = 4;
+
 template <typename Limit>
-inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
+inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas, int nsw = 0) {
   const int Npad = pad16(B);
   if (H % 64 || Npad > 256) return 0;
   const int RB = H / 32;
   int best = 0;
   for (int S = 1; S <= 8; S *= 2) {
     if (H % (64 * S)) continue;
-    const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
+    const RecurLayout L = recur_layout(G, H, Npad, S, NPL, nsw);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
     if ((Npad + 8 * S - 1) / (8 * S) > RMAXCELLS) continue;
+    if (nsw && (Npad + 8 * S - 1) / (8 * S) > 4) continue;  // streaming variant: <= 4 cells per thread
     if (D * RB * S > max_ctas(S)) continue;
     best = S;  // increasing S -> larger grid; keep the largest that fits
   }
   return best;
+}
+
+// Resident W_hh when possible, else the W-streaming variant.  *nsw = ring depth (0 = resident).
+template <typename Limit>
+inline int plan_split(int G, int H, int B, int D, int NPL, Limit max_ctas, int* nsw) {
+  int S = choose_split(G, H, B, D, NPL, max_ctas, 0);
+  *nsw = 0;
+  if (!S) {
+    S = choose_split(G, H, B, D, NPL, max_ctas, kSW);
+    *nsw = S ? kSW : 0;
+  }
+  return S;
 }
 
 // Batch slice of the recurrence: the largest equal split of B whose slice
@@ -47,7 +64,8 @@ inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas) {
 inline int batch_slice(int G, int H, int B, int D, int NPL) {
   for (int n = 1; n <= B; ++n) {
     const int Bs = (B + n - 1) / n;
-    if (Bs <= 256 && choose_split(G, H, Bs, D, NPL, static_cta_limit) > 0) return Bs;
+    int nsw;
+    if (Bs <= 256 && plan_split(G, H, Bs, D, NPL, static_cta_limit, &nsw) > 0) return Bs;
     if (Bs <= 16) break;
   }
   return 0;
@@ -282,7 +300,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   static bool init = false;
   std::string err;
   if (!init) {
-    if (set_smem(recur_tc_kernel<G, NPL, 1>, kSmemMax, err)) return 0;
+    if (set_smem(recur_tc_kernel<G, NPL, 1, 0>, kSmemMax, err)) return 0;
     init = true;
   }
   if (smem > kSmemMax) return 0;
@@ -298,7 +316,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL, 1>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL, 1, 0>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -310,18 +328,18 @@ inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
   return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
 }
 
-template <int G, int NPL, int CELLS>
+template <int G, int NPL, int CELLS, int NSW>
 inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
                         int S, size_t smem, cudaStream_t s, std::string& err) {
   static bool init = false;
   int rc;
   if (!init) {
-    if ((rc = set_smem(recur_tc_kernel<G, NPL, CELLS>, kSmemMax, err))) return rc;
+    if ((rc = set_smem(recur_tc_kernel<G, NPL, CELLS, NSW>, kSmemMax, err))) return rc;
     init = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.D * a.RB * S);
-  cfg.blockDim = dim3(kRecurThreads);
+  cfg.blockDim = dim3(kRecurThreads + (NSW ? 32 : 0));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -332,7 +350,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL, CELLS>, &cfg);
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL, CELLS, NSW>, &cfg);
   if (e != cudaSuccess) {
     err = std::string("cudaOccupancyMaxActiveClusters: ") + cudaGetErrorString(e);
     return 2;
@@ -342,7 +360,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
           std::to_string(S) + ", device fits " + std::to_string(nclusters);
     return 3;
   }
-  e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL, CELLS>, w0, w1, hm, a);
+  e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL, CELLS, NSW>, w0, w1, hm, a);
   if (e != cudaSuccess) {
     err = std::string("recur_tc_kernel launch: ") + cudaGetErrorString(e);
     return 2;
@@ -376,11 +394,18 @@ inline int dispatch_cells(int G, int NPL, int cells, F&& f, std::string& err) {
 inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, int sms,
                             cudaStream_t s, std::string& err) {
   (void)sms;
+  int nsw_try = 0;  // ring depth the limit is evaluated for
   auto limit = [&](int S_) -> int {
-    const size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL).total;
+    const size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total;
     return max_coresident_ctas(G, NPL, S_, sm_);
   };
-  const int S = choose_split(G, a.H, a.B, a.D, NPL, limit);
+  int nsw = 0;
+  int S = choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
+  if (!S) {
+    nsw_try = kSW;
+    S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);
+    nsw = S ? kSW : 0;
+  }
   if (!S) {
     err = "no feasible tensor-core split for this shape";
     return 3;
@@ -392,11 +417,22 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D, a.Npad, err);
   if (rc) return rc;
-  const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL).total;
+  const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL, nsw).total;
   int cells = 1;
   while (cells * (kEpiThreads / (32 / S)) < a.Npad) cells *= 2;
+  if (nsw) {  // streaming variant: instantiated for <= 4 cells per thread
+    return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) -> int {
+      if constexpr (decltype(c_)::value <= 4) {
+        return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value, kSW>(w0, w1, hm, a, S, smem,
+                                                                                                  s, err);
+      } else {
+        err = "W-streaming recurrence supports at most 4 cells per thread";
+        return 3;
+      }
+    }, err);
+  }
   return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) {
-    return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value>(w0, w1, hm, a, S, smem, s, err);
+    return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value, 0>(w0, w1, hm, a, S, smem, s, err);
   }, err);
 }
 

@@ -61,21 +61,26 @@ __device__ __forceinline__ unsigned long long globaltimer() {
       a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 16 + (phase)] = globaltimer();             \
   } while (0)
 
+constexpr int kMaxSW = 8;  // W-streaming ring depth limit
+
 struct RecurLayout {
   int nch;        // K chunks per CTA
   size_t w_off, h_off, red_off, bar_off, total;
 };
 
-__host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int S, int NPL) {
+// nsw = 0: the CTA's W_hh slice is resident (NPL planes x nch chunks);
+// nsw > 0: W_hh does not fit on chip and streams through an nsw-stage ring of
+// [NPL planes x 128 rows x 64 k] chunks, re-read from L2 every step.
+__host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int S, int NPL, int nsw = 0) {
   RecurLayout L;
   const int KS = H / S;
   L.nch = KS / 64;
   size_t off = 0;
-  L.w_off = off;   off += (size_t)NPL * L.nch * 128 * 128;
+  L.w_off = off;   off += (size_t)NPL * (nsw ? nsw : L.nch) * 128 * 128;
   L.h_off = off;   off += (size_t)L.nch * Npad * 128;  // one h plane
   L.red_off = off; off += (size_t)G * 32 * (Npad + 4) * 4;
   off = (off + 15) / 16 * 16;
-  L.bar_off = off; off += 8 * (5 + RMAXCH) + 16;
+  L.bar_off = off; off += 8 * (5 + RMAXCH + 1 + 2 * kMaxSW) + 16;
   L.total = off;  // dynamic smem starts 1024-aligned (checked in-kernel)
   return L;
 }
@@ -102,7 +107,7 @@ __device__ __forceinline__ void cluster_wait() {
 //                  owners over DSMEM, cluster barrier, then finish the gates of
 //                  the CTA's own units (c, h in registers), publish h_t planes
 //                  and release the chunk counter.
-constexpr int kRecurThreads = 256;
+constexpr int kRecurThreads = 256;  // + one W-producer warp in the streaming variant
 constexpr int kEpiThreads = 256;
 
 // tcgen05 instruction descriptor, kind::f16 with fp16 A/B and f32 D
@@ -121,15 +126,15 @@ __device__ __forceinline__ uint16_t h_operand(float h) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(h));
 }
 
-template <int G, int NPL, int CELLS>
-__global__ void __launch_bounds__(kRecurThreads, 1)
+template <int G, int NPL, int CELLS, int NSW>
+__global__ void __launch_bounds__(kRecurThreads + 32, 1)
     recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                     const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 atoms need 1024-B alignment
   const int H = a.H, B = a.B, Npad = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
-  const RecurLayout L = recur_layout(G, H, Npad, S, NPL);
+  const RecurLayout L = recur_layout(G, H, Npad, S, NPL, NSW);
   const int nch = L.nch;
   const int KS = H / S;
   const int UO = 32 / S;  // units finished by each rank
@@ -141,6 +146,8 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   uint64_t* acc_full = bars + 1;
   uint64_t* h_full = bars + 5;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + RMAXCH);
+  uint64_t* wfull = bars + 5 + RMAXCH + 1;   // streaming ring (NSW > 0)
+  uint64_t* wempty = wfull + kMaxSW;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = (int)ptx::cluster_rank();
@@ -166,6 +173,10 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
     ptx::mbar_init(w_full, 1);
     ptx::mbar_init(acc_full, 1);
     for (int c = 0; c < nch; ++c) ptx::mbar_init(&h_full[c], 1);
+    for (int i = 0; i < NSW; ++i) {
+      ptx::mbar_init(&wfull[i], 1);
+      ptx::mbar_init(&wempty[i], 1);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_dyn(tmem_slot, tcols);
@@ -175,7 +186,7 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   // resident W_hh slice: NPL planes x nch chunks of [128 rows x 64 k]
-  if (warp == 0 && ptx::elect_one()) {
+  if (NSW == 0 && warp == 0 && ptx::elect_one()) {
     ptx::mbar_arrive_expect_tx(w_full, (uint32_t)(NPL * nch * 128 * 128));
     for (int p = 0; p < NPL; ++p)
       for (int c = 0; c < nch; ++c)
@@ -183,10 +194,26 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   }
   __syncwarp();
 
+  // streaming variant: warp 8 keeps the W ring NSW chunks ahead of the MMAs.
+  // Ring item gi = s*nch + c holds chunk c (the same weights every step).
+  const int total_items = T * nch;
+  int w_next = 0;  // next ring item to load (warp 8 lane 0)
+  auto w_produce_until = [&](int last_item) {
+    for (; w_next <= last_item && w_next < total_items; ++w_next) {
+      const int slot = w_next % NSW, c = w_next % nch;
+      if (w_next >= NSW) ptx::mbar_wait(&wempty[slot], ((w_next / NSW) - 1) & 1);
+      ptx::mbar_arrive_expect_tx(&wfull[slot], (uint32_t)(NPL * 128 * 128));
+      for (int p = 0; p < NPL; ++p)
+        ptx::tma_load_3d(sW + ((size_t)slot * NPL + p) * 128 * 64, tmW, &wfull[slot], q * KS + c * 64, rb * 128, p);
+    }
+  };
+
   // owner cells: unit u_loc in [0, UO), batch rows b = b0 + k*bstep, k < CELLS
+  // (threads of the W-producer warp own no cells)
   const int e = threadIdx.x;
+  const bool owner = e < kEpiThreads;
   const int u_loc = e % UO;
-  const int b0 = e / UO;
+  const int b0 = owner ? e / UO : (1 << 20);  // non-owners: every row index out of range
   const int bstep = kEpiThreads / UO;
   const int unit = rb * 32 + q * UO + u_loc;
   float c_reg[CELLS], h_reg[CELLS], xq[CELLS][G];
@@ -232,7 +259,7 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
   const bool split = (Npad % 32) == 0;
   const int ncol = split ? Npad / 2 : Npad;
   const int col0 = split ? (warp >> 2) * ncol : 0;
-  const bool active = sub < G && (split || warp >= 4);
+  const bool active = warp < 8 && sub < G && (split || warp >= 4);
   const uint32_t red_remote =
       ptx::mapa(ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride), (uint32_t)(lane / UO));
 
@@ -257,26 +284,33 @@ __global__ void __launch_bounds__(kRecurThreads, 1)
         }
       }
       __syncwarp();
+    } else if (NSW && warp == 8) {
+      // keep the W ring NSW items ahead: this step's chunks, then the next step's first NSW
+      if (lane == 0) w_produce_until((s + 1) * nch + NSW - 1);
+      __syncwarp();
     } else if (warp == 1) {
       if (ptx::elect_one()) {
-        if (s == 0) ptx::mbar_wait(w_full, 0);
+        if (NSW == 0 && s == 0) ptx::mbar_wait(w_full, 0);
         HS_TRACE(13);
         for (int c = 0; c < nch; ++c) {
+          const int gi = s * nch + c, wslot = NSW ? gi % NSW : 0;
+          if (NSW) ptx::mbar_wait(&wfull[wslot], (gi / NSW) & 1);
           ptx::mbar_wait(&h_full[c], s & 1);
           ptx::tc_fence_after();
           if (c == 0) HS_TRACE(15);
           if (c == nch - 1) HS_TRACE(14);
-          const __nv_bfloat16* wh = sW + (size_t)c * 128 * 64;
+          const __nv_bfloat16* wh = NSW ? sW + (size_t)wslot * NPL * 128 * 64 : sW + (size_t)c * 128 * 64;
           const __nv_bfloat16* hh = sH + (size_t)c * Npad * 64;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
                              (c | kk) != 0);
             if (NPL == 2) {  // + W_lo · h
-              const __nv_bfloat16* wl = wh + (size_t)nch * 128 * 64;
+              const __nv_bfloat16* wl = wh + (size_t)(NSW ? 1 : nch) * 128 * 64;
               ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
             }
           }
+          if (NSW) ptx::mma_commit(&wempty[wslot]);  // ring slot free once these MMAs have read it
         }
         ptx::mma_commit(acc_full);
         HS_TRACE(2);

@@ -44,6 +44,7 @@ ABI_SYMBOLS = (
     "hs_last_error",
     "hs_rnn_last_launch_count",
     "hs_rnn_resolve_algo",
+    "hs_rnn_plan",
     "hs_rnn_workspace",
     "hs_rnn_packed_size",
     "hs_rnn_pack_weights",
@@ -170,6 +171,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_last_launch_count.restype = ctypes.c_int
     lib.hs_rnn_resolve_algo.argtypes = [pd, ctypes.POINTER(i32)]
     lib.hs_rnn_workspace.argtypes = [pd, ctypes.POINTER(sz)]
+    lib.hs_rnn_plan.argtypes = [pd, ctypes.POINTER(i32)]
     lib.hs_rnn_packed_size.argtypes = [pd, ctypes.POINTER(sz)]
     lib.hs_rnn_pack_weights.argtypes = [pd, pvp, pvp, pvp, pvp, vp, sz, vp]
     lib.hs_rnn_forward_packed.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, ctypes.POINTER(ctypes.c_float)]
@@ -268,6 +270,13 @@ class RNNExecutor:
                     ctypes.byref(self.desc), *arrs, self.packed.data_ptr(), self.packed.numel(), stream.cuda_stream
                 ),
             )
+
+    def plan(self) -> dict:
+        """The library's execution plan for this model (``hs_rnn_plan``)."""
+        info = (ctypes.c_int32 * 8)()
+        _check(self.lib, "hs_rnn_plan", self.lib.hs_rnn_plan(ctypes.byref(self.desc), info))
+        return {"algo": ALGO_NAMES[info[0]], "cluster": info[1], "w_ring": info[2], "batch_slices": info[3],
+                "small_kernel": bool(info[4]), "w_hh_resident": info[0] == 2 and info[2] == 0}
 
     def last_launch_count(self) -> int:
         """Kernels the library launched in the last forward call on this

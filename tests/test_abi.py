@@ -81,3 +81,26 @@ def test_forward_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         rnn.RNNExecutor(CONFIGS["c1"], rnn.init_weights(CONFIGS["c1"]))
+
+
+def test_plan_query_without_gpu():
+    """hs_rnn_plan is static (no device needed): the BASELINE configs map to
+    the kernels DESIGN.md describes."""
+    import ctypes
+
+    from paper_2307_11339_b200 import CONFIGS
+    from paper_2307_11339_b200.rnn import load_library, make_desc
+
+    lib = load_library()
+
+    def plan(spec):
+        info = (ctypes.c_int32 * 8)()
+        assert lib.hs_rnn_plan(ctypes.byref(make_desc(spec)), info) == 0
+        return list(info)
+
+    c1, c2, c3, c4, c5 = (plan(CONFIGS[k]) for k in ("c1", "c2", "c3", "c4", "c5"))
+    assert c1[0] == 1 and c1[4] == 1 and c1[1] in (4, 8, 16)  # SIMT small-shape cluster kernel
+    assert c2[0] == 2 and c2[2] == 0 and c2[1] == 4          # tensor cores, W_hh resident, S = 4
+    assert c3[0] == 2 and c3[2] == 0
+    assert c4[0] == 2 and c4[2] > 0                          # W_hh 64 MiB/layer: streamed ring
+    assert c5[0] == 2 and c5[3] > 1                          # bf16, batch sliced on one GPU
