@@ -29,8 +29,8 @@ struct SmallArgs {
   const float* w_hh[2];          // per dir [G*H][H] fp32
   const float* bias_x[2];        // per dir [G*H] (b_ih (+ b_hh for LSTM))
   const float* bias_h[2];        // per dir [G*H] (GRU b_hh) or nullptr
-  const float* h0[2];            // per dir [B][H]
-  const float* c0[2];
+  const float* h0[2];            // per dir [B][H], nullptr = zeros
+  const float* c0[2];            // nullptr = zeros
   float* y;                      // [T][B][D*H]
   float* hn[2];                  // per dir [B][H]
   float* cn[2];
@@ -114,11 +114,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) recur_cluster_small(const Sm
     }
 #pragma unroll 4
     for (int i = tid; i < B * H4; i += kSmallThreads)
-      reinterpret_cast<float4*>(hbuf)[i] = __ldg(reinterpret_cast<const float4*>(a.h0[d]) + i);
+      reinterpret_cast<float4*>(hbuf)[i] =
+          a.h0[d] ? __ldg(reinterpret_cast<const float4*>(a.h0[d]) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int i = tid; i < U * B; i += kSmallThreads) {
     const int u = i / B, b = i % B;
-    cst[i] = G == 4 ? a.c0[d][(size_t)b * H + q * U + u] : 0.f;
+    cst[i] = (G == 4 && a.c0[d]) ? a.c0[d][(size_t)b * H + q * U + u] : 0.f;
   }
   for (int r = tid; r < rows; r += kSmallThreads) {
     const int grow = (r / U) * H + q * U + r % U;

@@ -585,14 +585,15 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
   if (algo == HS_ALGO_TC) return tc_forward(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, layer_ms, ov);
   const size_t DBH = (size_t)m.D * m.B * m.H;
   float* zeros = at<float>(ws, wl.zeros);
-  if (!h0 || (m.G == 4 && !c0)) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
+  const int C = pl.ld[0].whh ? small_cluster(m) : 0;
+  // the small-shape kernel zero-fills missing initial states itself (one launch fewer)
+  if (!C && (!h0 || (m.G == 4 && !c0))) HS_CUDA(cudaMemsetAsync(zeros, 0, DBH * sizeof(float), s));
   cudaEvent_t evs[2 * 64 + 1];
   const int nev = layer_ms ? 2 * m.L + 1 : 0;
   for (int i = 0; i < nev; ++i) HS_CUDA(cudaEventCreate(&evs[i]));
   if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
   const size_t TB = (size_t)m.T * m.B;
   const float* in = x;
-  const int C = pl.ld[0].whh ? small_cluster(m) : 0;
   for (int l = 0; l < m.L; ++l) {
     float* out = (l == m.L - 1) ? y : at<float>(ws, (l & 1) ? wl.act1 : wl.act0);
     const int Il = m.in_size(l);
@@ -608,8 +609,8 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
         sa.w_hh[d] = at<float>(packed, lp.whh);
         sa.bias_x[d] = at<float>(packed, lp.bias_x);
         sa.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
-        sa.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
-        sa.c0[d] = c0 ? c0 + (size_t)ld * m.B * m.H : zeros + (size_t)d * m.B * m.H;
+        sa.h0[d] = h0 ? h0 + (size_t)ld * m.B * m.H : nullptr;  // nullptr: zeros
+        sa.c0[d] = c0 ? c0 + (size_t)ld * m.B * m.H : nullptr;
         sa.hn[d] = hn + (size_t)ld * m.B * m.H;
         sa.cn[d] = cn ? cn + (size_t)ld * m.B * m.H : at<float>(ws, wl.cst) + (size_t)d * m.B * m.H;
       }

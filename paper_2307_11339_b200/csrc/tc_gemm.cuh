@@ -20,10 +20,14 @@ namespace tc {
 
 constexpr int GBM = 128;
 constexpr int GBK = 64;
-constexpr int GSTAGES = 4;
+// BN = 256: 4-stage ring, one CTA per SM.  BN = 128: 3-stage ring and two
+// CTAs per SM, so one CTA's epilogue overlaps the other's MMAs.
+template <int BN>
+constexpr int gemm_stages() { return BN == 256 ? 4 : 3; }
 
 template <int BN>
 struct GemmSmem {
+  static constexpr int GSTAGES = gemm_stages<BN>();
   __nv_bfloat16 a[GSTAGES][GBM * GBK];
   __nv_bfloat16 b[GSTAGES][BN * GBK];
   uint64_t full[GSTAGES];
@@ -43,7 +47,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 
 // tmA: 3D {K, M, 2 planes} bf16, box {64, 128, 1}; tmB: 3D {K, N, 2}, box {64, BN, 1}.
 template <int BN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
     gemm_xproj_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int npass) {
   extern __shared__ uint8_t smem_raw[];
@@ -52,6 +56,7 @@ __global__ void __launch_bounds__(256, 1)
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
   const int nk = K / GBK;
   const int nkb = npass * nk;
+  constexpr int GSTAGES = gemm_stages<BN>();
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
@@ -125,6 +130,133 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, BN);
+  }
+}
+
+// Persistent form of K1: one CTA per SM walks the (M/128) x (N/256) output
+// tiles (tile = blockIdx.x + k * gridDim.x).  The TMA ring runs across tile
+// boundaries and the accumulator is double-buffered in TMEM (2 x 256 of the
+// 512 columns), so the epilogue of tile j (TMEM -> +bias -> global) overlaps
+// the MMAs of tile j+1 — the non-persistent kernel leaves the tensor pipe idle
+// during every epilogue.
+struct GemmPSmem {
+  static constexpr int ST = 4;
+  __nv_bfloat16 a[ST][GBM * GBK];
+  __nv_bfloat16 b[ST][256 * GBK];
+  uint64_t full[ST];
+  uint64_t empty[ST];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
+  uint32_t tmem_base;
+};
+
+constexpr size_t gemm_p_smem_bytes() { return sizeof(GemmPSmem) + 1024; }
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_xproj_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int npass) {
+  constexpr int BN = 256, ST = GemmPSmem::ST;
+  extern __shared__ uint8_t smem_raw[];
+  GemmPSmem& sm = *reinterpret_cast<GemmPSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = K / GBK, nkb = npass * nk;
+  const int tiles_n = N / BN, tiles = ((M + GBM - 1) / GBM) * tiles_n;
+  const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < ST; ++s) {
+      ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&sm.tmem_full[b], 1);
+      ptx::mbar_init(&sm.tmem_empty[b], 4);  // one arrive per epilogue warp
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(&sm.tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      for (int j = 0; j < my_tiles; ++j) {
+        const int t = blockIdx.x + j * gridDim.x;
+        const int m0 = (t / tiles_n) * GBM, n0 = (t % tiles_n) * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int g = j * nkb + kb, st = g % ST;
+          if (g >= ST) ptx::mbar_wait(&sm.empty[st], ((g / ST) - 1) & 1);
+          const int pass = kb / nk, kk = kb % nk;
+          const int pa = pass == 2 ? 1 : 0, pb = pass == 1 ? 1 : 0;
+          ptx::mbar_arrive_expect_tx(&sm.full[st], (GBM + BN) * GBK * 2);
+          ptx::tma_load_3d(sm.a[st], &tmA, &sm.full[st], kk * GBK, m0, pa);
+          ptx::tma_load_3d(sm.b[st], &tmB, &sm.full[st], kk * GBK, n0, pb);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (ptx::elect_one()) {
+      const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
+      for (int j = 0; j < my_tiles; ++j) {
+        const int buf = j & 1;
+        if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);  // epilogue drained it
+        ptx::tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int g = j * nkb + kb, st = g % ST;
+          ptx::mbar_wait(&sm.full[st], (g / ST) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k) {
+            const uint64_t ad = ptx::sdesc_k_sw128(sm.a[st] + k * 16);
+            const uint64_t bd = ptx::sdesc_k_sw128(sm.b[st] + k * 16);
+            ptx::mma_bf16_ss(acc, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&sm.empty[st]);
+        }
+        ptx::mma_commit(&sm.tmem_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int t = blockIdx.x + j * gridDim.x;
+      const int m0 = (t / tiles_n) * GBM, n0 = (t % tiles_n) * BN;
+      const int buf = j & 1;
+      ptx::mbar_wait(&sm.tmem_full[buf], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int row = m0 + sub * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(buf * BN + c * 32), v);
+        if (row < M) {
+          const int n = n0 + c * 32;
+          float* dst = C + (size_t)row * N + n;
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias + n + q);
+            *reinterpret_cast<float4*>(dst + q) =
+                make_float4(v[q] + bb.x, v[q + 1] + bb.y, v[q + 2] + bb.z, v[q + 3] + bb.w);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&sm.tmem_empty[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
   }
 }
 

@@ -78,7 +78,11 @@ inline bool supports(int G, int H, int B, int I0, int DH, int D = 1, int NPL = 2
 
 inline bool profitable(int G, int H, int B, int T) { return H >= 256 && B >= 4 && (long)T * B >= 128; }
 
-inline int gemm_bn(int N) { return N % 256 == 0 ? 256 : 128; }
+inline int gemm_bn(int N) {
+  static const char* env = getenv("HS_GEMM_BN");  // experiments: force the N tile
+  if (env) return atoi(env) == 128 || N % 256 ? 128 : 256;
+  return N % 256 == 0 ? 256 : 128;
+}
 
 // packed planes per layer-direction: W_ih [2][G*H][I] bf16, W_hh row-block packed [2][H/32*128][H] bf16
 inline size_t wih_plane_elems(int G, int H, int I) { return (size_t)G * H * I; }
@@ -261,7 +265,20 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   if (rc) return rc;
   dim3 grid(N / BN, (M + GBM - 1) / GBM);
   cudaError_t e;
-  if (BN == 256) {
+  static const char* np_env = getenv("HS_GEMM_NONPERSISTENT");  // A/B runs
+  if (BN == 256 && !np_env) {
+    static bool initp = false;
+    static int sms = 0;
+    if (!initp) {
+      if ((rc = set_smem(gemm_xproj_persistent, gemm_p_smem_bytes(), err))) return rc;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      initp = true;
+    }
+    const int tiles = (int)(grid.x * grid.y);
+    gemm_xproj_persistent<<<tiles < sms ? tiles : sms, 256, gemm_p_smem_bytes(), s>>>(ta, tb, bias, C, M, N, K, npass);
+  } else if (BN == 256) {
     static bool init = false;
     if (!init) { if ((rc = set_smem(gemm_xproj_kernel<256>, gemm_smem_bytes<256>(), err))) return rc; init = true; }
     gemm_xproj_kernel<256><<<grid, 256, gemm_smem_bytes<256>(), s>>>(ta, tb, bias, C, M, N, K, npass);
@@ -400,10 +417,13 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
     return max_coresident_ctas(G, NPL, S_, sm_);
   };
   int nsw = 0;
-  int S = choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
+  static const char* force_sw = getenv("HS_FORCE_STREAM");  // experiments: stream W even if it fits
+  int S = force_sw ? 0 : choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
   if (!S) {
     nsw_try = kSW;
     S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);
+    static const char* force_s = getenv("HS_FORCE_S");
+    if (force_s && S) S = atoi(force_s) < S ? atoi(force_s) : S;
     nsw = S ? kSW : 0;
   }
   if (!S) {
