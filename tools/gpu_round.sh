@@ -5,6 +5,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+for c in c3 c4 c5; do timeout 900 python bench.py --config $c --no-cpu-baseline --steps 5 > gpurun_out/b_$c.log 2>&1; done
+timeout 300 python tools/c1_latency.py > gpurun_out/c1_latency.json 2>/dev/null
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:recur_tc_kernel -s 2 -c 1 -o gpurun_out/recur_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_recur.log 2>&1
