@@ -153,3 +153,14 @@ def test_launch_count_reports_library_kernels():
     small = RNNExecutor(CONFIGS["c1"], init_weights(CONFIGS["c1"]))
     small.forward(make_input(CONFIGS["c1"]).to(small.device))
     assert small.last_launch_count() == 1  # the whole layer in one cluster launch
+
+
+@pytest.mark.parametrize("spec", [
+    RNNSpec("gru", 1, 96, 9, 5, input=40, dirs=2),   # small-shape cluster kernel, GRU, bidirectional
+    RNNSpec("lstm", 3, 32, 20, 64),                  # small-shape kernel at its batch limit
+    RNNSpec("lstm", 1, 256, 6, 2),                   # 16-CTA cluster, 64 gate rows per CTA
+], ids=lambda s: f"{s.cell}{s.layers}x{s.hidden}T{s.seq}B{s.batch}d{s.dirs}")
+def test_small_cluster_kernel_shapes(spec):
+    ex, got, ref = run_both(spec, seed=3)
+    assert ex.plan()["small_kernel"]
+    assert max_err(got, ref) <= TOL_F32

@@ -70,3 +70,34 @@ def test_tc_c5_width_sharded_batch():
     err = run(CONFIGS["c5"].with_(seq=12, batch=32))
     print(f"c5 shard bf16 max-abs {err:.3e}")
     assert err <= 1e-2
+
+
+EDGE = [
+    RNNSpec("lstm", 1, 256, 1, 1, algo="tc"),                    # T = 1, B = 1
+    RNNSpec("lstm", 2, 64, 5, 1, input=128, dirs=2, algo="tc"),  # smallest TC hidden, bidirectional
+    RNNSpec("lstm", 3, 192, 4, 17, input=64, algo="tc"),         # ragged batch (Npad 32), odd depth
+    RNNSpec("gru", 1, 256, 6, 128, dtype="bf16"),                # bf16 GRU, full M=128 batch
+]
+
+
+@pytest.mark.parametrize("spec", EDGE, ids=lambda s: f"{s.cell}{s.layers}x{s.hidden}T{s.seq}B{s.batch}d{s.dirs}{s.dtype}")
+def test_tc_edge_shapes(spec):
+    err = run(spec)
+    print(f"edge max-abs {err:.3e}")
+    assert err <= (1e-2 if spec.dtype == "bf16" else 1e-4)
+
+
+def test_tc_initial_states_bidirectional():
+    """h0/c0 on the tensor-core path, both directions (state indexing l*D + d)."""
+    spec = RNNSpec("lstm", 2, 128, 7, 12, dirs=2, algo="tc")
+    w = init_weights(spec, 7)
+    x = make_input(spec, 8)
+    gen = torch.Generator().manual_seed(11)
+    h0 = (torch.rand((4, 12, 128), generator=gen) - 0.5)
+    c0 = (torch.rand((4, 12, 128), generator=gen) - 0.5)
+    ex = RNNExecutor(spec, w)
+    y, hn, cn = ex.forward(x.to(ex.device), h0.to(ex.device), c0.to(ex.device))
+    ref = rnn_forward_ref("lstm", x.double().numpy(), [{k: v.double().numpy() for k, v in d.items()} for d in w],
+                          h0.double().numpy(), c0.double().numpy(), dirs=2)
+    for g, r in zip((y, hn, cn), ref):
+        assert float(np.abs(g.cpu().double().numpy() - r).max()) <= 1e-4
