@@ -519,7 +519,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
           const __nv_bfloat16* wihn = at<__nv_bfloat16>(packed, lpn.tc);
           float* xpn = xpb[(l + 1) & 1] + (size_t)d * TB * m.G * m.H;
           rc = gemm_planes(xpl + r0 * In, wihn, at<float>(packed, lpn.bias_x), xpn + r0 * m.G * m.H, (int)nr,
-                           m.G * m.H, In, NPL == 2 ? 3 : 1, gs, g_err, TB * In);
+                           m.G * m.H, In, NPL == 2 ? 3 : 1, gs, g_err, TB * In, /*persistent=*/false);
           if (rc) return rc;
         }
       }

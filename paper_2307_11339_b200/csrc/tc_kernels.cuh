@@ -256,8 +256,12 @@ inline int set_smem(K kernel, size_t bytes, std::string& err) {
 
 // K1 on planes: A planes [2][M][K], W_ih planes [2][N][K]
 // (a_pstride: element distance between the A hi and lo planes; 0 = M*K)
+// persistent = false: one CTA per tile.  Required when the launch shares the
+// GPU with a running persistent recurrence: a persistent GEMM's tile lists are
+// fixed per CTA, so its CTAs queued behind the recurrence would hold back their
+// tiles until the recurrence ends; one-tile CTAs trickle onto the free SMs.
 inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const float* bias, float* C, int M, int N, int K,
-                       int npass, cudaStream_t s, std::string& err, size_t a_pstride = 0) {
+                       int npass, cudaStream_t s, std::string& err, size_t a_pstride = 0, bool persistent = true) {
   CUtensorMap ta, tb;
   const int BN = gemm_bn(N);
   int rc = make_map3(&ta, apl, K, M, 2, GBM, err, a_pstride);
@@ -266,7 +270,7 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   dim3 grid(N / BN, (M + GBM - 1) / GBM);
   cudaError_t e;
   static const char* np_env = getenv("HS_GEMM_NONPERSISTENT");  // A/B runs
-  if (BN == 256 && !np_env) {
+  if (BN == 256 && persistent && !np_env) {
     static bool initp = false;
     static int sms = 0;
     if (!initp) {
