@@ -473,7 +473,18 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       for (int i = 0; i < 12; ++i) HS_CUDA(cudaEventCreate(&dbg_ev[i]));
       HS_CUDA(cudaEventRecord(dbg_ev[0], s));
     }
-    if (nsl == 1) {
+    // two batch-half groups per CTA (tc_recur2.cuh) when the batch is large
+    // enough for both chains to carry work: c2 (B=64) 6.85 -> 6.58 us/step;
+    // slower at B=32 (c3: 4.25 -> 4.68 ms).  HS_TWO_GROUPS=0/1 overrides.
+    static const char* two_env = getenv("HS_TWO_GROUPS");
+    const bool two_req = two_env ? atoi(two_env) == 1 : m.B >= 64;
+    const bool two = nsl == 1 && two_req && choose_split2(m.G, m.H, m.B, m.D, NPL) > 0;
+    if (two) {
+      static const char* off_env = getenv("HS_TG_OFFSET_NS");
+      a.group_offset_ns = off_env ? (unsigned int)atoi(off_env) : 0u;
+      rc = recurrence_layer2(m.G, NPL, whh, a, s, g_err);
+      if (rc) return rc;
+    } else if (nsl == 1) {
       rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
       if (rc) return rc;
     } else {
@@ -504,7 +515,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     if (drain && dbg) HS_CUDA(cudaEventRecord(dbg_ev[1], s));
     if (feed_next) {
       // K1 of layer l+1, chunk k, once every CTA has finished step s_need
-      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);  // two-group: one increment per group
       const int In = m.in_size(l + 1);
       const int nk = m.T < 8 ? m.T : 8;
       for (int k = 0; k < nk; ++k) {
@@ -526,7 +537,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     }
     if (drain) {
       // y chunk [t0, t1) is final once every CTA has finished step s_need
-      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S);
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);  // two-group: one increment per group
       WaitValue32Fn wait = nsl == 1 ? wait_value_fn() : nullptr;
       if (!wait && (rc = join(s, ov->cs_out))) return rc;  // no stream memory ops / sliced: drain after the kernel
       const int nco = m.T < 16 ? m.T : 16;

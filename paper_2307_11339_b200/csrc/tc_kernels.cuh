@@ -10,6 +10,7 @@
 #include "simt_kernels.cuh"
 #include "tc_gemm.cuh"
 #include "tc_recur.cuh"
+#include "tc_recur2.cuh"
 
 namespace hs {
 namespace tc {
@@ -457,6 +458,92 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   }
   return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) {
     return launch_recur<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value, 0>(w0, w1, hm, a, S, smem, s, err);
+  }, err);
+}
+
+
+// ------------------------------------------- two-group recurrence (tc_recur2.cuh)
+// K-split for two batch halves per CTA; 0 = infeasible.
+inline int choose_split2(int G, int H, int B, int D, int NPL) {
+  if (B < 2 || H % 64) return 0;
+  const int Np = pad16((B + 1) / 2);
+  if (Np > 64) return 0;
+  const int RB = H / 32;
+  int best = 0;
+  for (int S = 1; S <= 8; S *= 2) {
+    if (H % (64 * S)) continue;
+    const Recur2Layout L = recur2_layout(G, H, Np, S, NPL);
+    if (L.nch > RMAXCH || L.total > kSmemMax) continue;
+    if ((Np + (128 / (32 / S)) - 1) / (128 / (32 / S)) > 4) continue;  // <= 4 cells per thread
+    if (D * RB * S > static_cta_limit(S)) continue;
+    best = S;
+  }
+  return best;
+}
+
+template <int G, int NPL, int CELLS>
+inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
+                         int S, size_t smem, cudaStream_t s, std::string& err) {
+  static bool init = false;
+  int rc;
+  if (!init) {
+    if ((rc = set_smem(recur_tc2_kernel<G, NPL, CELLS>, kSmemMax, err))) return rc;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.D * a.RB * S);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc2_kernel<G, NPL, CELLS>, &cfg);
+  if (e != cudaSuccess || nclusters * S < (int)cfg.gridDim.x) {
+    err = "two-group recurrent kernel cannot be co-resident";
+    return 3;
+  }
+  e = cudaLaunchKernelEx(&cfg, recur_tc2_kernel<G, NPL, CELLS>, w0, w1, hm, a);
+  if (e != cudaSuccess) {
+    err = std::string("recur_tc2_kernel launch: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  ++g_launch_count;
+  return 0;
+}
+
+// a.B = full batch; a.Npad is set to the per-group padding; a.S / a.RB filled in.
+inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, cudaStream_t s,
+                             std::string& err) {
+  const int S = choose_split2(G, a.H, a.B, a.D, NPL);
+  if (!S) {
+    err = "no feasible two-group split";
+    return 3;
+  }
+  a.S = S;
+  a.RB = a.H / 32;
+  a.Npad = pad16((a.B + 1) / 2);
+  CUtensorMap w0, w1, hm;
+  int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
+  if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
+  if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * kNG, a.Npad, err);
+  if (rc) return rc;
+  const size_t smem = recur2_layout(G, a.H, a.Npad, S, NPL).total;
+  int cells = 1;
+  while (cells * (128 / (32 / S)) < a.Npad) cells *= 2;
+  return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) -> int {
+    if constexpr (decltype(c_)::value <= 4) {
+      return launch_recur2<decltype(g_)::value, decltype(npl_)::value, decltype(c_)::value>(w0, w1, hm, a, S, smem, s,
+                                                                                             err);
+    } else {
+      err = "two-group recurrence supports at most 4 cells per thread";
+      return 3;
+    }
   }, err);
 }
 

@@ -46,6 +46,7 @@ struct TcRecurArgs {
   unsigned int* counters;       // [D][S]
   unsigned long long* trace;    // optional [grid][kTraceSteps][16] %globaltimer stamps (debug)
   unsigned int* progress;       // optional [T]: progress[s] counts CTAs whose outputs of step s are in memory
+  unsigned int group_offset_ns; // two-group kernel: initial phase offset of group 1 (0 = none)
 };
 
 constexpr int kTraceSteps = 64;

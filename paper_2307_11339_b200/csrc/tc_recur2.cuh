@@ -1,0 +1,324 @@
+// K2/K3, two-group form of the cluster K-split recurrence (tc_recur.cuh).
+//
+// The batch rows of a sequence batch are independent recurrences, so each CTA
+// runs TWO of them — batch halves ("groups") — side by side on the same
+// resident W_hh slice: warps 0-3 serve group 0, warps 4-7 group 1, each with
+// its own producer lane, MMA lane, TMEM accumulator, h_{t-1} staging, partial
+// buffer, readiness counters and barriers.  A step of the recurrence is a
+// latency chain (h all-gather through L2, MMA, DSMEM reduce-scatter, gates,
+// release); with two independent chains in flight, one group's waits overlap
+// the other group's work.  The cluster-wide reduce-scatter is therefore
+// synchronised per group with mbarriers instead of barrier.cluster:
+//   red_full[g]   owner side: S ranks x 4 sending warps arrive (release) after
+//                 their st.shared::cluster partial stores
+//   red_free[g]   sender side: S ranks x 4 owner warps arrive (relaxed) after
+//                 reading the previous step's partials
+//   tmem_free[g]  the group's 4 warps drained the accumulator
+// Numerics are identical to tc_recur.cuh (fp16 W hi/lo x fp16 h, f32 TMEM).
+#pragma once
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "tc_recur.cuh"
+
+namespace hs {
+namespace tc {
+
+constexpr int kNG = 2;  // groups per CTA
+
+struct Recur2Layout {
+  int nch;
+  size_t w_off, h_off, red_off, bar_off, total;
+  size_t h_group, red_group;  // bytes per group
+};
+
+// Np = padded rows of ONE group
+__host__ __device__ inline Recur2Layout recur2_layout(int G, int H, int Np, int S, int NPL) {
+  Recur2Layout L;
+  const int KS = H / S;
+  L.nch = KS / 64;
+  size_t off = 0;
+  L.w_off = off;   off += (size_t)NPL * L.nch * 128 * 128;
+  L.h_group = (size_t)L.nch * Np * 128;
+  L.h_off = off;   off += kNG * L.h_group;
+  L.red_group = (size_t)G * 32 * (Np + 4) * 4;
+  L.red_off = off; off += kNG * L.red_group;
+  off = (off + 15) / 16 * 16;
+  // per group: acc_full, red_full, red_free, tmem_free, h_full[RMAXCH]; + w_full, tmem slot
+  L.bar_off = off; off += 8 * (2 + kNG * (4 + RMAXCH)) + 16;
+  L.total = off;
+  return L;
+}
+
+template <int G, int NPL, int CELLS>
+__global__ void __launch_bounds__(256, 1)
+    recur_tc2_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
+                     const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem_raw) & 1023) __trap();
+  // a.B = total batch, a.Npad = padded rows of one group (Bh = ceil(B/2) rows each)
+  const int H = a.H, B = a.B, Np = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
+  const int Bh = (B + 1) / 2;
+  const Recur2Layout L = recur2_layout(G, H, Np, S, NPL);
+  const int nch = L.nch;
+  const int KS = H / S;
+  const int UO = 32 / S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp >> 2;           // group of this warp
+  const int sub = warp & 3;            // TMEM lane quarter
+  const int eg = threadIdx.x & 127;    // thread index within the group
+  const int Bg = grp == 0 ? Bh : B - Bh;  // real rows of this group
+  const int brow0 = grp * Bh;              // first global batch row of the group
+
+  __nv_bfloat16* sW = reinterpret_cast<__nv_bfloat16*>(smem + L.w_off);
+  __nv_bfloat16* sH = reinterpret_cast<__nv_bfloat16*>(smem + L.h_off + grp * L.h_group);
+  float* red = reinterpret_cast<float*>(smem + L.red_off + grp * L.red_group);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* w_full = bars;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1);
+  uint64_t* gb = bars + 2 + grp * (4 + RMAXCH);  // this group's barriers
+  uint64_t* acc_full = gb;
+  uint64_t* red_full = gb + 1;
+  uint64_t* red_free = gb + 2;
+  uint64_t* tmem_free = gb + 3;
+  uint64_t* h_full = gb + 4;
+
+  const int q = (int)ptx::cluster_rank();
+  const int cl = blockIdx.x / S;
+  const int d = cl / RB;
+  const int rb = cl % RB;
+  const CUtensorMap* tmW = d == 0 ? &tmW0 : &tmW1;
+  const int GH = G * H;
+  const int rstride = Np + 4;
+  const uint32_t tcols_g = Np <= 32 ? 32 : Np <= 64 ? 64 : 128;
+  const uint32_t tcols = 2 * tcols_g;
+  constexpr int kCtrStride = 32;
+  const int nchunk_all = H / 64;
+  unsigned int* ctr_g = a.counters + (size_t)grp * D * nchunk_all * kCtrStride;
+  unsigned int* my_counter = ctr_g + (d * nchunk_all + (rb * 32) / 64) * kCtrStride;
+  const unsigned int* in_counter = ctr_g + (d * nchunk_all + (q * KS) / 64) * kCtrStride;
+  const unsigned int per_round = 2u * (unsigned int)S;
+  const size_t slab = (size_t)Np * H;  // hbuf elements per (buf, d, group)
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(tmW);
+    ptx::tma_prefetch(&tmH);
+    ptx::mbar_init(w_full, 1);
+    for (int g2 = 0; g2 < kNG; ++g2) {
+      uint64_t* b2 = bars + 2 + g2 * (4 + RMAXCH);
+      ptx::mbar_init(b2 + 0, 1);                       // acc_full
+      ptx::mbar_init(b2 + 1, (uint32_t)(S * 4));       // red_full
+      ptx::mbar_init(b2 + 2, (uint32_t)(S * 4));       // red_free
+      ptx::mbar_init(b2 + 3, 4);                       // tmem_free
+      for (int c = 0; c < nch; ++c) ptx::mbar_init(b2 + 4 + c, 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_dyn(tmem_slot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot + (uint32_t)(grp * tcols_g);
+
+  if (warp == 0 && ptx::elect_one()) {
+    ptx::mbar_arrive_expect_tx(w_full, (uint32_t)(NPL * nch * 128 * 128));
+    for (int p = 0; p < NPL; ++p)
+      for (int c = 0; c < nch; ++c)
+        ptx::tma_load_3d(sW + ((size_t)p * nch + c) * 128 * 64, tmW, w_full, q * KS + c * 64, rb * 128, p);
+  }
+  __syncwarp();
+
+  // owner cells of this group: unit u_loc, group rows b = b0 + k*bstep
+  const int u_loc = eg % UO;
+  const int b0 = eg / UO;
+  const int bstep = 128 / UO;
+  const int unit = rb * 32 + q * UO + u_loc;
+  float c_reg[CELLS], h_reg[CELLS], xq[CELLS][G];
+  float wsc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) wsc[g] = a.whh_scale[d][rb * 128 + g * 32 + q * UO + u_loc];
+  float bias_r = 0.f, bias_z = 0.f, bias_n = 0.f;
+  if (G == 3 && a.bias_h[d]) {
+    bias_r = a.bias_h[d][unit];
+    bias_z = a.bias_h[d][H + unit];
+    bias_n = a.bias_h[d][2 * H + unit];
+  }
+  auto load_xproj = [&](int step) {
+    const int tt = d == 0 ? step : T - 1 - step;
+    const float* __restrict__ xp = a.xproj[d] + (size_t)tt * a.Bst * GH + unit;
+#pragma unroll
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+#pragma unroll
+      for (int g = 0; g < G; ++g) xq[k][g] = b < Bg ? __ldg(xp + (size_t)(brow0 + b) * GH + g * H) : 0.f;
+    }
+  };
+  auto group_release = [&](unsigned int* ctr) {  // the group's 4 warps, then one release
+    ptx::named_bar(1 + grp, 128);
+    if (eg == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < CELLS; ++k) {
+    c_reg[k] = 0.f;
+    h_reg[k] = 0.f;
+    const int b = b0 + k * bstep;
+    if (b < Bg) {
+      h_reg[k] = a.h0[d][(size_t)(brow0 + b) * H + unit];
+      if (G == 4) c_reg[k] = a.c0[d][(size_t)(brow0 + b) * H + unit];
+      a.hbuf[((size_t)(0 * D + d) * kNG + grp) * slab + (size_t)b * H + unit] = h_operand<NPL>(h_reg[k]);
+    }
+  }
+  ptx::fence_proxy_async_global();
+  load_xproj(0);
+  group_release(my_counter);
+  cluster_arrive();  // every CTA's barriers initialised before any remote op
+  cluster_wait();
+
+  const uint32_t idesc = NPL == 2 ? idesc_f16_f32(128, Np) : ptx::idesc_bf16_f32(128, Np);
+  const bool active = sub < G;
+  const int dst_rank = lane / UO;
+  const uint32_t red_remote =
+      ptx::mapa(ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride), (uint32_t)dst_rank);
+
+  for (int s = 0; s < T; ++s) {
+    const int t = d == 0 ? s : T - 1 - s;
+    const int buf_in = s % 3, buf_out = (s + 1) % 3;
+    const bool last = s == T - 1;
+    if (sub == 0) {  // producer of this group
+      if (lane == 0) {
+        if (s == 0 && grp == 1 && a.group_offset_ns) {  // start group 1 out of phase
+          const unsigned long long t0 = globaltimer();
+          while (globaltimer() - t0 < a.group_offset_ns) {
+          }
+        }
+        const unsigned int target = per_round * (unsigned int)(s + 1);
+        for (int c = 0; c < nch; ++c) {
+          unsigned int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter + c * kCtrStride) : "memory");
+          } while (seen < target);
+          ptx::fence_proxy_async_global();
+          ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Np * 128));
+          ptx::tma_load_3d(sH + (size_t)c * Np * 64, &tmH, &h_full[c], q * KS + c * 64, 0,
+                           (buf_in * D + d) * kNG + grp);
+        }
+      }
+      __syncwarp();
+    } else if (sub == 1) {  // MMA issuer of this group
+      if (ptx::elect_one()) {
+        if (s == 0) ptx::mbar_wait(w_full, 0);
+        else ptx::mbar_wait(tmem_free, (s - 1) & 1);
+        for (int c = 0; c < nch; ++c) {
+          ptx::mbar_wait(&h_full[c], s & 1);
+          ptx::tc_fence_after();
+          const __nv_bfloat16* wh = sW + (size_t)c * 128 * 64;
+          const __nv_bfloat16* hh = sH + (size_t)c * Np * 64;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
+                             (c | kk) != 0);
+            if (NPL == 2) {
+              const __nv_bfloat16* wl = wh + (size_t)nch * 128 * 64;
+              ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
+            }
+          }
+        }
+        ptx::mma_commit(acc_full);
+      }
+      __syncwarp();
+    }
+    // 1. drain TMEM, reduce-scatter the group's partial gates to the unit owners
+    ptx::mbar_wait(acc_full, s & 1);
+    ptx::tc_fence_after();
+    if (active) {
+      if (s > 0) ptx::mbar_wait_cluster(red_free, (s - 1) & 1);  // owners read step s-1's partials
+      for (int c16 = 0; c16 < Np / 16; ++c16) {
+        float v[16];
+        ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + c16 * 16, v);
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          ptx::st_cluster_v4(red_remote + (uint32_t)(c16 * 16 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+    }
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(tmem_free);
+    // every warp (padding-row warps of GRU included) arrives once on each owner
+    if (lane < S) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(red_full), (uint32_t)lane));
+    ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units landed
+    // 2. owner: gates -> h_t (critical path)
+#pragma unroll
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+      if (b >= Np) break;
+      float pre[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float* rp = red + ((size_t)g * UO + u_loc) * rstride + b;
+        float acc = rp[0];
+#pragma unroll
+        for (int sr = 1; sr < 8; ++sr)
+          if (sr < S) acc += rp[(size_t)sr * G * UO * rstride];
+        pre[g] = acc * wsc[g];
+      }
+      float h;
+      if (G == 4) {
+        const float ig = sigmoid_fast(pre[0] + xq[k][0]), fg = sigmoid_fast(pre[1] + xq[k][1]);
+        const float gg = tanh_fast(pre[2] + xq[k][2]), og = sigmoid_fast(pre[3] + xq[k][3]);
+        const float cnew = fg * c_reg[k] + ig * gg;
+        c_reg[k] = cnew;
+        h = og * tanh_fast(cnew);
+      } else {
+        const float r = sigmoid_fast(xq[k][0] + pre[0] + bias_r);
+        const float z = sigmoid_fast(xq[k][1] + pre[1] + bias_z);
+        const float n = tanh_fast(xq[k][2] + r * (pre[2] + bias_n));
+        h = (1.f - z) * n + z * h_reg[k];
+      }
+      h_reg[k] = h;
+      if (!last && b < Bg)
+        a.hbuf[((size_t)(buf_out * D + d) * kNG + grp) * slab + (size_t)b * H + unit] = h_operand<NPL>(h);
+    }
+    // partials read (values consumed above): senders may refill the buffer
+    __syncwarp();
+    if (lane < S) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(red_free), (uint32_t)lane));
+    if (!last) {
+      ptx::fence_proxy_async_global();
+      group_release(my_counter);
+    }
+    // 3. off the critical path: outputs, final state, next step's XP
+#pragma unroll
+    for (int k = 0; k < CELLS; ++k) {
+      const int b = b0 + k * bstep;
+      if (b >= Bg) continue;
+      const float hv = h_reg[k];
+      const size_t yidx = ((size_t)t * a.Bst + brow0 + b) * D * H + (size_t)d * H + unit;
+      if (a.y) a.y[yidx] = hv;
+      if (a.ypl) {
+        __nv_bfloat16 hi, lo;
+        ptx::split_bf16(hv, hi, lo);
+        a.ypl[yidx] = hi;
+        a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
+      }
+      if (last) {
+        a.hn[d][(size_t)(brow0 + b) * H + unit] = hv;
+        if (G == 4) a.cn[d][(size_t)(brow0 + b) * H + unit] = c_reg[k];
+      }
+    }
+    if (a.progress) {  // y of step s in memory: one increment per group per CTA
+      ptx::named_bar(1 + grp, 128);
+      if (eg == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s) : "memory");
+    }
+    if (!last) load_xproj(s + 1);
+  }
+  cluster_arrive();  // no CTA leaves while peers may still write its partials / barriers
+  cluster_wait();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(*tmem_slot, tcols);
+  }
+}
+
+}  // namespace tc
+}  // namespace hs
