@@ -9,8 +9,10 @@
 // release); with two independent chains in flight, one group's waits overlap
 // the other group's work.  The cluster-wide reduce-scatter is therefore
 // synchronised per group with mbarriers instead of barrier.cluster:
-//   red_full[g]   owner side: S ranks x 4 sending warps arrive (release) after
-//                 their st.shared::cluster partial stores
+//   red_full[g]   owner side: the 4 local warps arrive after writing their own
+//                 rows; the S-1 peers' slices arrive as bulk copies
+//                 (cp.async.bulk shared::cta -> shared::cluster) whose
+//                 complete_tx settles the expected byte count
 //   red_free[g]   sender side: S ranks x 4 owner warps arrive (relaxed) after
 //                 reading the previous step's partials
 //   tmem_free[g]  the group's 4 warps drained the accumulator
@@ -27,8 +29,8 @@ constexpr int kNG = 2;  // groups per CTA
 
 struct Recur2Layout {
   int nch;
-  size_t w_off, h_off, red_off, bar_off, total;
-  size_t h_group, red_group;  // bytes per group
+  size_t w_off, h_off, red_off, stage_off, bar_off, total;
+  size_t h_group, red_group, stage_group;  // bytes per group
 };
 
 // Np = padded rows of ONE group
@@ -42,6 +44,9 @@ __host__ __device__ inline Recur2Layout recur2_layout(int G, int H, int Np, int 
   L.h_off = off;   off += kNG * L.h_group;
   L.red_group = (size_t)G * 32 * (Np + 4) * 4;
   L.red_off = off; off += kNG * L.red_group;
+  // outgoing partials for the S-1 peers, laid out like their destination regions
+  L.stage_group = (size_t)(S - 1) * G * (32 / S) * (Np + 4) * 4;
+  L.stage_off = off; off += kNG * L.stage_group;
   off = (off + 15) / 16 * 16;
   // per group: acc_full, red_full, red_free, tmem_free, h_full[RMAXCH]; + w_full, tmem slot
   L.bar_off = off; off += 8 * (2 + kNG * (4 + RMAXCH)) + 16;
@@ -73,6 +78,8 @@ __global__ void __launch_bounds__(256, 1)
   __nv_bfloat16* sW = reinterpret_cast<__nv_bfloat16*>(smem + L.w_off);
   __nv_bfloat16* sH = reinterpret_cast<__nv_bfloat16*>(smem + L.h_off + grp * L.h_group);
   float* red = reinterpret_cast<float*>(smem + L.red_off + grp * L.red_group);
+  float* stage = reinterpret_cast<float*>(smem + L.stage_off + grp * L.stage_group);
+  const uint32_t region_floats = (uint32_t)(G * UO * (Np + 4));  // one sender's rows in an owner's buffer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* w_full = bars;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1);
@@ -107,12 +114,14 @@ __global__ void __launch_bounds__(256, 1)
     for (int g2 = 0; g2 < kNG; ++g2) {
       uint64_t* b2 = bars + 2 + g2 * (4 + RMAXCH);
       ptx::mbar_init(b2 + 0, 1);                       // acc_full
-      ptx::mbar_init(b2 + 1, (uint32_t)(S * 4));       // red_full
+      ptx::mbar_init(b2 + 1, 5);                       // red_full: 4 local warps + the owner's expect_tx
       ptx::mbar_init(b2 + 2, (uint32_t)(S * 4));       // red_free
       ptx::mbar_init(b2 + 3, 4);                       // tmem_free
       for (int c = 0; c < nch; ++c) ptx::mbar_init(b2 + 4 + c, 1);
     }
     ptx::fence_mbar_init();
+    for (int g2 = 0; g2 < kNG; ++g2)  // phase 0: the S-1 peers' bulk copies
+      ptx::mbar_arrive_expect_tx(bars + 2 + g2 * (4 + RMAXCH) + 1, (uint32_t)((S - 1) * G * UO * (Np + 4) * 4));
   }
   if (warp == 2) ptx::tmem_alloc_dyn(tmem_slot, tcols);
   ptx::tc_fence_before();
@@ -177,8 +186,10 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t idesc = NPL == 2 ? idesc_f16_f32(128, Np) : ptx::idesc_bf16_f32(128, Np);
   const bool active = sub < G;
   const int dst_rank = lane / UO;
-  const uint32_t red_remote =
-      ptx::mapa(ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride), (uint32_t)dst_rank);
+  // this lane's row: in my own buffer (dst == me) or in the staging slot of peer dst
+  float* part_row = dst_rank == q ? red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride
+                                  : stage + (size_t)(dst_rank < q ? dst_rank : dst_rank - 1) * region_floats +
+                                        ((size_t)sub * UO + lane % UO) * rstride;
 
   for (int s = 0; s < T; ++s) {
     const int t = d == 0 ? s : T - 1 - s;
@@ -186,6 +197,7 @@ __global__ void __launch_bounds__(256, 1)
     const bool last = s == T - 1;
     if (sub == 0) {  // producer of this group
       if (lane == 0) {
+        if (grp == 0) HS_TRACE(0);
         if (s == 0 && grp == 1 && a.group_offset_ns) {  // start group 1 out of phase
           const unsigned long long t0 = globaltimer();
           while (globaltimer() - t0 < a.group_offset_ns) {
@@ -197,6 +209,8 @@ __global__ void __launch_bounds__(256, 1)
           do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter + c * kCtrStride) : "memory");
           } while (seen < target);
+          if (grp == 0 && c == 0) HS_TRACE(1);
+          if (grp == 0 && c == nch - 1) HS_TRACE(12);
           ptx::fence_proxy_async_global();
           ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Np * 128));
           ptx::tma_load_3d(sH + (size_t)c * Np * 64, &tmH, &h_full[c], q * KS + c * 64, 0,
@@ -224,28 +238,51 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         ptx::mma_commit(acc_full);
+        if (grp == 0) HS_TRACE(2);
       }
       __syncwarp();
     }
     // 1. drain TMEM, reduce-scatter the group's partial gates to the unit owners
     ptx::mbar_wait(acc_full, s & 1);
     ptx::tc_fence_after();
+    if (threadIdx.x == 64) HS_TRACE(3);
+    // partials go to LOCAL shared memory (own rows -> my buffer, peers' rows ->
+    // staging), then one thread moves each peer's slice with a bulk copy whose
+    // complete_tx lands on the peer's red_full: no per-thread DSMEM stores and
+    // no release fence on the sender side
     if (active) {
-      if (s > 0) ptx::mbar_wait_cluster(red_free, (s - 1) & 1);  // owners read step s-1's partials
+      if (threadIdx.x == 64) HS_TRACE(7);
       for (int c16 = 0; c16 < Np / 16; ++c16) {
         float v[16];
         ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + c16 * 16, v);
 #pragma unroll
         for (int j = 0; j < 16; j += 4)
-          ptx::st_cluster_v4(red_remote + (uint32_t)(c16 * 16 + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+          *reinterpret_cast<float4*>(part_row + c16 * 16 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       }
     }
+    if (threadIdx.x == 64) HS_TRACE(8);
     ptx::tc_fence_before();
+    ptx::fence_proxy_async_smem();  // staging writes -> the bulk copy (async proxy)
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(tmem_free);
-    // every warp (padding-row warps of GRU included) arrives once on each owner
-    if (lane < S) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(red_full), (uint32_t)lane));
+    if (lane == 0) ptx::mbar_arrive(red_full);  // my own rows are in place
+    ptx::named_bar(1 + grp, 128);               // the group's staging is complete
+    if (eg == 0) {
+      if (s > 0) ptx::mbar_wait_cluster(red_free, (s - 1) & 1);  // peers read step s-1's partials
+      for (int r = 0; r < S; ++r) {
+        if (r == q) continue;
+        const float* src = stage + (size_t)(r < q ? r : r - 1) * region_floats;
+        const uint32_t dst = ptx::mapa(ptx::smem_u32(red + (size_t)q * region_floats), (uint32_t)r);
+        ptx::bulk_s2cluster(dst, src, region_floats * 4u, ptx::mapa(ptx::smem_u32(red_full), (uint32_t)r));
+      }
+      ptx::bulk_commit();
+      ptx::bulk_wait_read0();  // staging reusable (next step's drain comes long after)
+    }
+    if (threadIdx.x == 64) HS_TRACE(4);
     ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units landed
+    if (threadIdx.x == 64) HS_TRACE(5);
+    if (eg == 0 && !last)  // next phase: the peers' bulk copies of step s+1
+      ptx::mbar_arrive_expect_tx(red_full, (uint32_t)((S - 1) * region_floats * 4));
     // 2. owner: gates -> h_t (critical path)
 #pragma unroll
     for (int k = 0; k < CELLS; ++k) {
@@ -278,6 +315,7 @@ __global__ void __launch_bounds__(256, 1)
       if (!last && b < Bg)
         a.hbuf[((size_t)(buf_out * D + d) * kNG + grp) * slab + (size_t)b * H + unit] = h_operand<NPL>(h);
     }
+    if (threadIdx.x == 64) HS_TRACE(6);
     // partials read (values consumed above): senders may refill the buffer
     __syncwarp();
     if (lane < S) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(red_free), (uint32_t)lane));
@@ -285,6 +323,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::fence_proxy_async_global();
       group_release(my_counter);
     }
+    if (threadIdx.x == 0) HS_TRACE(10);
     // 3. off the critical path: outputs, final state, next step's XP
 #pragma unroll
     for (int k = 0; k < CELLS; ++k) {
