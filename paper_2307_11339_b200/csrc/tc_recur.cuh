@@ -66,7 +66,7 @@ constexpr int kMaxSW = 8;  // W-streaming ring depth limit
 
 struct RecurLayout {
   int nch;        // K chunks per CTA
-  size_t w_off, h_off, red_off, bar_off, total;
+  size_t w_off, h_off, red_off, stage_off, bar_off, total;
 };
 
 // nsw = 0: the CTA's W_hh slice is resident (NPL planes x nch chunks);
@@ -80,6 +80,8 @@ __host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int 
   L.w_off = off;   off += (size_t)NPL * (nsw ? nsw : L.nch) * 128 * 128;
   L.h_off = off;   off += (size_t)L.nch * Npad * 128;  // one h plane
   L.red_off = off; off += (size_t)G * 32 * (Npad + 4) * 4;
+  // outgoing partials for the S-1 peers, laid out like their destination regions
+  L.stage_off = off; off += (size_t)(S - 1) * G * (32 / S) * (Npad + 4) * 4;
   off = (off + 15) / 16 * 16;
   L.bar_off = off; off += 8 * (5 + RMAXCH + 1 + 2 * kMaxSW) + 16;
   L.total = off;  // dynamic smem starts 1024-aligned (checked in-kernel)
@@ -142,9 +144,13 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
   __nv_bfloat16* sW = reinterpret_cast<__nv_bfloat16*>(smem + L.w_off);
   __nv_bfloat16* sH = reinterpret_cast<__nv_bfloat16*>(smem + L.h_off);
   float* red = reinterpret_cast<float*>(smem + L.red_off);
+  float* stage = reinterpret_cast<float*>(smem + L.stage_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* w_full = bars;
   uint64_t* acc_full = bars + 1;
+  uint64_t* red_full = bars + 2;   // 8 local warps + the owner's expect_tx for the peers' bulk copies
+  uint64_t* red_free = bars + 3;   // S ranks x 8 owner warps finished reading the partials
+  uint64_t* tmem_free = bars + 4;  // 8 warps drained the accumulator
   uint64_t* h_full = bars + 5;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + RMAXCH);
   uint64_t* wfull = bars + 5 + RMAXCH + 1;   // streaming ring (NSW > 0)
@@ -178,7 +184,11 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
       ptx::mbar_init(&wfull[i], 1);
       ptx::mbar_init(&wempty[i], 1);
     }
+    ptx::mbar_init(red_full, 9);
+    ptx::mbar_init(red_free, (uint32_t)(S * 8));
+    ptx::mbar_init(tmem_free, 8);
     ptx::fence_mbar_init();
+    ptx::mbar_arrive_expect_tx(red_full, (uint32_t)((S - 1) * G * UO * (Npad + 4) * 4));  // phase 0
   }
   if (warp == 2) ptx::tmem_alloc_dyn(tmem_slot, tcols);
   ptx::tc_fence_before();
@@ -252,7 +262,8 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
   load_xproj(0);
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
-  cluster_arrive();
+  cluster_arrive();  // every CTA's barriers initialised before any remote op
+  cluster_wait();
 
   // f32 mode: fp16 W hi/lo x fp16 h; bf16 mode: bf16 x bf16
   const uint32_t idesc = NPL == 2 ? idesc_f16_f32(128, Npad) : ptx::idesc_bf16_f32(128, Npad);
@@ -261,8 +272,12 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
   const int ncol = split ? Npad / 2 : Npad;
   const int col0 = split ? (warp >> 2) * ncol : 0;
   const bool active = warp < 8 && sub < G && (split || warp >= 4);
-  const uint32_t red_remote =
-      ptx::mapa(ptx::smem_u32(red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride), (uint32_t)(lane / UO));
+  const uint32_t region_floats = (uint32_t)(G * UO * rstride);  // one sender's rows in an owner's buffer
+  const int dst_rank = lane / UO;
+  // this lane's partial row: in my own buffer (dst == me) or in peer dst's staging slot
+  float* part_row = dst_rank == q ? red + ((size_t)(q * G + sub) * UO + lane % UO) * rstride
+                                  : stage + (size_t)(dst_rank < q ? dst_rank : dst_rank - 1) * region_floats +
+                                        ((size_t)sub * UO + lane % UO) * rstride;
 
   for (int s = 0; s < T; ++s) {
     const int t = d == 0 ? s : T - 1 - s;
@@ -292,6 +307,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
     } else if (warp == 1) {
       if (ptx::elect_one()) {
         if (NSW == 0 && s == 0) ptx::mbar_wait(w_full, 0);
+        if (s > 0) ptx::mbar_wait(tmem_free, (s - 1) & 1);  // every warp drained step s-1
         HS_TRACE(13);
         for (int c = 0; c < nch; ++c) {
           const int gi = s * nch + c, wslot = NSW ? gi % NSW : 0;
@@ -318,8 +334,9 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
       }
       __syncwarp();
     }
-    cluster_wait();  // peers finished reading last step's partials
-    // 1. drain TMEM, reduce-scatter partial gates to the unit owners
+    // 1. drain TMEM into LOCAL shared memory (own rows -> my buffer, peers'
+    //    rows -> staging); one thread then moves each peer's slice with a bulk
+    //    copy whose complete_tx lands on the peer's red_full
     ptx::mbar_wait(acc_full, s & 1);
     ptx::tc_fence_after();
     if (e == 128) HS_TRACE(3);
@@ -330,13 +347,34 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
         ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(sub * 32) << 16) + col, v);
 #pragma unroll
         for (int j = 0; j < 16; j += 4)
-          ptx::st_cluster_v4(red_remote + (uint32_t)(col + j) * 4u, v[j], v[j + 1], v[j + 2], v[j + 3]);
+          *reinterpret_cast<float4*>(part_row + col + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       }
     }
     ptx::tc_fence_before();
+    if (warp < 8) {
+      ptx::fence_proxy_async_smem();  // staging writes -> the bulk copy (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(tmem_free);
+        ptx::mbar_arrive(red_full);  // my own rows are in place
+      }
+      ptx::named_bar(1, 256);  // staging complete
+      if (e == 0) {
+        if (s > 0) ptx::mbar_wait_cluster(red_free, (s - 1) & 1);  // peers read step s-1's partials
+        for (int r = 0; r < S; ++r) {
+          if (r == q) continue;
+          const float* src = stage + (size_t)(r < q ? r : r - 1) * region_floats;
+          const uint32_t dst = ptx::mapa(ptx::smem_u32(red + (size_t)q * region_floats), (uint32_t)r);
+          ptx::bulk_s2cluster(dst, src, region_floats * 4u, ptx::mapa(ptx::smem_u32(red_full), (uint32_t)r));
+        }
+        ptx::bulk_commit();
+        ptx::bulk_wait_read0();  // staging reusable
+      }
+    }
     if (e == 128) HS_TRACE(4);
-    cluster_arrive();
-    cluster_wait();  // all partials for my units are in my shared memory
+    ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units are in my shared memory
+    if (e == 0 && !last)  // next phase: the peers' bulk copies of step s+1
+      ptx::mbar_arrive_expect_tx(red_full, (uint32_t)((S - 1) * region_floats * 4));
     if (e == 128) HS_TRACE(5);
     // 2. owner: gates -> h_t planes (critical path)
 #pragma unroll
@@ -372,7 +410,10 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
       }
     }
     if (e == 128) HS_TRACE(6);
-    cluster_arrive_relaxed();  // partial-sum buffer fully read: peers may refill it
+    if (warp < 8) {  // partials read (values consumed above): peers may refill the buffer
+      __syncwarp();
+      if (lane < S) ptx::mbar_arrive_remote_relaxed(ptx::mapa(ptx::smem_u32(red_free), (uint32_t)lane));
+    }
     ptx::fence_proxy_async_global();
     __syncthreads();  // all h_t stores of this CTA issued
     if (e == 128) HS_TRACE(8);
@@ -404,6 +445,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
     if (!last) load_xproj(s + 1);
     if (e == 0) HS_TRACE(11);
   }
+  cluster_arrive();  // no CTA leaves while peers may still copy into it / arrive on its barriers
   cluster_wait();
   ptx::tc_fence_before();
   __syncthreads();
