@@ -207,24 +207,32 @@ def reference_planner():
 
 
 def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic):
-    """Roofline of the dominant kernel, the recurrence.  W_hh resident on chip
-    (SMEM): bound by the tensor pipe — achieved = algorithmic recurrent FLOPs
-    / time vs the measured bf16 peak.  W_hh streamed every step (it does not
-    fit on chip, e.g. c4): bound by memory — algorithmic bytes per forward =
-    T*L*D*(W_hh at 4 B/weight + xproj row reads + y writes) vs measured HBM."""
+    """Roofline of the dominant kernel, the recurrence: t_roof = max(FLOPs /
+    tensor peak, bytes / HBM bandwidth), so frac = max of the two fractions and
+    `bound` names the larger.  FLOPs: the algorithmic recurrent FLOPs.  Bytes:
+    the W_hh bytes that must cross the memory system — zero when W_hh stays
+    resident in shared memory; when it is streamed (plan w_ring > 0, e.g. c4)
+    every step of every batch slice re-reads it (4 B/weight in fp32 mode as
+    fp16 hi+lo, 2 B in bf16 mode) — plus the xproj reads and y writes."""
     common = {"kernel": f"recurrent wavefront ({algo})", "kernel_ms_per_forward": rec_ms,
               "gemm_ms_per_forward": gemm_ms, "traffic": traffic}
-    if plan.get("w_ring"):
-        G, H, B, T = spec.G, spec.hidden, spec.batch, spec.seq
-        per_step = 4.0 * G * H * H + 4.0 * B * G * H + 4.0 * B * H
-        nbytes = T * spec.layers * spec.dirs * per_step
-        gbs = nbytes / (rec_ms / 1e3) / 1e9
-        return dict(common, bound="hbm", achieved=gbs, peak=peaks["hbm_gbs"], unit="GB/s", frac=gbs / peaks["hbm_gbs"],
-                    algorithmic_bytes=nbytes, peak_source=f"{peaks['source']} HBM copy")
-    tf = rec_f / (rec_ms / 1e3) / 1e12
-    return dict(common, bound="tensor", achieved=tf, peak=peaks["bf16_tflops"], unit="TFLOP/s",
-                frac=tf / peaks["bf16_tflops"], algorithmic_flops=rec_f,
-                peak_source=f"{peaks['source']} dense bf16 (burst)")
+    sec = rec_ms / 1e3
+    tf = rec_f / sec / 1e12
+    f_tensor = tf / peaks["bf16_tflops"]
+    G, H, B, T = spec.G, spec.hidden, spec.batch, spec.seq
+    wbytes = (2.0 if spec.dtype == "bf16" else 4.0) * G * H * H
+    slices = max(1, plan.get("batch_slices", 1))
+    per_step = (wbytes * slices if plan.get("w_ring") else 0.0) + 4.0 * B * G * H + 4.0 * B * H
+    nbytes = T * spec.layers * spec.dirs * per_step
+    gbs = nbytes / sec / 1e9
+    f_hbm = gbs / peaks["hbm_gbs"]
+    tensor = dict(achieved=tf, peak=peaks["bf16_tflops"], unit="TFLOP/s", frac=f_tensor, algorithmic_flops=rec_f,
+                  peak_source=f"{peaks['source']} dense bf16 (burst)")
+    hbm = dict(achieved=gbs, peak=peaks["hbm_gbs"], unit="GB/s", frac=f_hbm, algorithmic_bytes=nbytes,
+               peak_source=f"{peaks['source']} HBM copy")
+    if f_hbm > f_tensor:
+        return dict(common, bound="hbm", **hbm, other={"bound": "tensor", **tensor})
+    return dict(common, bound="tensor", **tensor, other={"bound": "hbm", **hbm})
 
 
 def describe(spec) -> str:

@@ -9,7 +9,7 @@ for c in c3 c4 c5; do timeout 900 python bench.py --config $c --no-cpu-baseline 
 timeout 300 python tools/c1_latency.py > gpurun_out/c1_latency.json 2>/dev/null
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:recur_tc_kernel -s 2 -c 1 -o gpurun_out/recur_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_recur.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:recur_tc -s 2 -c 1 -o gpurun_out/recur_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_recur.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_xproj -s 2 -c 1 -o gpurun_out/gemm_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_gemm.log 2>&1
 timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_case.py > gpurun_out/racecheck.log 2>&1
 timeout 900 compute-sanitizer --tool synccheck python tools/sanitize_case.py > gpurun_out/synccheck.log 2>&1
