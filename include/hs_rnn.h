@@ -73,7 +73,10 @@ typedef struct hs_rnn_desc {
   int32_t batch;   /* B */
   int32_t dtype;   /* hs_dtype: F32 = fp32-exact (max-abs 1e-4), BF16 = opt-in */
   int32_t algo;    /* hs_algo */
-  int32_t reserved[7];
+  int32_t upload_chunks;  /* hs_rnn_forward_host: time chunks x is uploaded in (0 = 4).
+                            1 suits request streams (x already uploaded during the
+                            previous request); more chunks lower single-request latency */
+  int32_t reserved[6];
 } hs_rnn_desc;
 
 /* ABI version of the loaded library (HS_RNN_ABI_VERSION). */

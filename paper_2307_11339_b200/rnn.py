@@ -133,7 +133,8 @@ class _Desc(ctypes.Structure):
         ("batch", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
         ("algo", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("upload_chunks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
     ]
 
 
@@ -322,11 +323,13 @@ class RNNExecutor:
         return tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() if t is not None else None
                      for t in self.alloc_outputs())
 
-    def forward_host(self, x_host: torch.Tensor, h0=None, c0=None, out_host=None, staging=None):
+    def forward_host(self, x_host: torch.Tensor, h0=None, c0=None, out_host=None, staging=None, upload_chunks=0):
         """End-to-end forward on host tensors (``hs_rnn_forward_host``): the
         H2D upload of ``x`` and the D2H download of ``y`` overlap the compute
         on the tensor-core path.  Host tensors should be pinned.  Returns the
-        host ``(y, h_n, c_n)``; work is complete when the current stream is."""
+        host ``(y, h_n, c_n)``; work is complete when the current stream is.
+        ``upload_chunks``: time chunks x is uploaded in (0 = library default);
+        1 suits request streams, where the upload overlaps the previous request."""
         s = self.spec
         for name, t in (("x", x_host), ("h0", h0), ("c0", c0)):
             if t is not None and (t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous()):
@@ -338,6 +341,7 @@ class RNNExecutor:
             staging = self.alloc_staging()
         xd, (yd, hnd, cnd), state = staging
         ptr = lambda t: t.data_ptr() if t is not None else None
+        self.desc.upload_chunks = int(upload_chunks)
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device)
             _check(

@@ -64,7 +64,7 @@ class RNNServer:
         if tuple(req.x.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"request x has shape {tuple(req.x.shape)}, model expects {(s.seq, s.batch, s.I)}")
 
-    def _submit(self, req: InferenceRequest, slot: int) -> tuple[int, int]:
+    def _submit(self, req: InferenceRequest, slot: int, upload_chunks: int = 0) -> tuple[int, int]:
         """Enqueue one request on the current stream; returns (h2d, d2h) bytes."""
         ex = self.ex
         staging = self.staging[slot]
@@ -72,7 +72,7 @@ class RNNServer:
         if req.x.device.type == "cpu":
             h0 = req.h0.contiguous() if req.h0 is not None else None
             c0 = req.c0.contiguous() if req.c0 is not None else None
-            ex.forward_host(req.x.contiguous(), h0, c0, out_host=host_outs, staging=staging)
+            ex.forward_host(req.x.contiguous(), h0, c0, out_host=host_outs, staging=staging, upload_chunks=upload_chunks)
             h2d = sum(t.numel() * t.element_size() for t in (req.x, h0, c0) if t is not None)
         else:
             dev = ex.device
@@ -124,7 +124,8 @@ class RNNServer:
             slot = i % self.slots
             if pending[slot] is not None:
                 finish(slot)
-            h2d, d2h = self._submit(req, slot)
+            # in a stream the upload overlaps the previous request: one chunk
+            h2d, d2h = self._submit(req, slot, upload_chunks=1 if i else 0)
             h2d_total += h2d
             d2h_total += d2h
             ev = done[slot] or torch.cuda.Event()
