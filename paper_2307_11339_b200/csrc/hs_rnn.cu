@@ -517,7 +517,34 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       }
     }
     if (drain && dbg) HS_CUDA(cudaEventRecord(dbg_ev[1], s));
-    if (feed_next) {
+    static const char* chunked_env = getenv("HS_K1_CHUNKED");  // A/B: the fixed time-chunk schedule below
+    const bool dyn_k1 = feed_next && gemm_bn(m.G * m.H) == 256 && !(chunked_env && atoi(chunked_env) == 1);
+    if (dyn_k1) {
+      // K1 of layer l+1 as one dynamic-schedule launch (gemm_xproj_dyn): issued
+      // once every recurrence CTA has finished step 0 (so the recurrence is
+      // resident and cannot be starved of SMs), one CTA per SM; tiles are
+      // claimed in time order and each waits in-kernel for its rows
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);
+      const int In = m.in_size(l + 1);
+      CUresult r = wait_value_fn()(gs, reinterpret_cast<CUdeviceptr>(a.progress), ncta, 0 /*GEQ*/);
+      if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      unsigned int* claim = reinterpret_cast<unsigned int*>(tcws + tw.claim);
+      HS_CUDA(cudaMemsetAsync(claim, 0, sizeof(unsigned int), gs));
+      GemmDynArgs ga{};
+      const __nv_bfloat16* wpl[2] = {nullptr, nullptr};
+      for (int d = 0; d < m.D; ++d) {
+        const LayerPack& lpn = pl.ld[(l + 1) * m.D + d];
+        wpl[d] = at<__nv_bfloat16>(packed, lpn.tc);
+        ga.bias[d] = at<float>(packed, lpn.bias_x);
+        ga.C[d] = xpb[(l + 1) & 1] + (size_t)d * TB * m.G * m.H;
+      }
+      ga.M = (int)TB; ga.N = m.G * m.H; ga.K = In; ga.npass = NPL == 2 ? 3 : 1;
+      ga.D = m.D; ga.T = m.T; ga.B = m.B;
+      ga.claim = claim;
+      ga.progress = a.progress;
+      ga.ncta = ncta;
+      if ((rc = gemm_planes_dyn(xpl, TB * In, wpl, ga, di.sms, gs, g_err))) return rc;
+    } else if (feed_next) {
       // K1 of layer l+1, chunk k, once every CTA has finished step s_need
       const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);  // two-group: one increment per group
       const int In = m.in_size(l + 1);

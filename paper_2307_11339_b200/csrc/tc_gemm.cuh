@@ -260,6 +260,179 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dynamic-schedule K1 for the layer overlap: layer l+1's input projection
+// while layer l's recurrence is still running.  Tiles are claimed in time
+// order from one global counter (atomicAdd), unit t -> (M-tile m, direction
+// d, N-tile n), and the producer polls the recurrence's per-step progress
+// counter for the M-tile's last timestep before loading its rows.  Launched
+// with one CTA per SM once the recurrence is resident: the CTAs that find a
+// free SM (those the persistent recurrence leaves idle) start right away and
+// wait for rows as they are published; the rest start when the recurrence
+// exits and take the remaining tiles at full width.  Same pipeline as
+// gemm_xproj_persistent (TMA ring across tiles, double-buffered TMEM
+// accumulators), plus a 16-slot tile-id queue in shared memory (tq_full
+// mbarriers) from the producer to the MMA and epilogue warps.
+struct GemmDynArgs {
+  const float* bias[2];            // per direction [N]
+  float* C[2];                     // per direction [M, N]
+  int M, N, K, npass, D, T, B;
+  unsigned int* claim;             // zeroed before launch
+  const unsigned int* progress;    // [T] CTAs of the recurrence that finished step s
+  unsigned int ncta;               // progress[s] value meaning "step s complete everywhere"
+};
+
+struct GemmDSmem {
+  static constexpr int ST = 4, NQ = 16;
+  __nv_bfloat16 a[ST][GBM * GBK];
+  __nv_bfloat16 b[ST][256 * GBK];
+  uint64_t full[ST];
+  uint64_t empty[ST];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
+  uint64_t tq_full[NQ];
+  int tq[NQ];
+  uint32_t tmem_base;
+};
+
+constexpr size_t gemm_d_smem_bytes() { return sizeof(GemmDSmem) + 1024; }
+
+__global__ void __launch_bounds__(256, 1)
+    gemm_xproj_dyn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                   const __grid_constant__ CUtensorMap tmB1, const GemmDynArgs g) {
+  constexpr int BN = 256, ST = GemmDSmem::ST, NQ = GemmDSmem::NQ;
+  extern __shared__ uint8_t smem_raw[];
+  GemmDSmem& sm = *reinterpret_cast<GemmDSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = g.K / GBK, nkb = g.npass * nk;
+  const int tiles_n = g.N / BN, per_m = g.D * tiles_n;
+  const int tiles = ((g.M + GBM - 1) / GBM) * per_m;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB0);
+    if (g.D > 1) ptx::tma_prefetch(&tmB1);
+    for (int s = 0; s < ST; ++s) {
+      ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&sm.tmem_full[b], 1);
+      ptx::mbar_init(&sm.tmem_empty[b], 4);
+    }
+    for (int q = 0; q < NQ; ++q) ptx::mbar_init(&sm.tq_full[q], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(&sm.tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  // the queue slot of tile j is rewritten at j + NQ; the producer runs at most
+  // ST stages + 2 TMEM buffers (< NQ tiles) ahead of the epilogue
+  auto next_tile = [&](int j) -> int {
+    ptx::mbar_wait(&sm.tq_full[j % NQ], (uint32_t)((j / NQ) & 1));
+    return sm.tq[j % NQ];
+  };
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      for (int j = 0;; ++j) {
+        int t = (int)atomicAdd(g.claim, 1u);
+        if (t >= tiles) t = -1;
+        sm.tq[j % NQ] = t;
+        ptx::mbar_arrive(&sm.tq_full[j % NQ]);
+        if (t < 0) break;
+        const int mt = t / per_m, d = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
+        const int m0 = mt * GBM;
+        // rows [m0, m0+128) hold timesteps [t0, t1); they are final once the
+        // recurrence finished step s_need (a backward direction runs T-1 .. 0)
+        const int t0 = m0 / g.B, t1 = min(g.T, (m0 + GBM + g.B - 1) / g.B);
+        const int s_need = g.D == 1 ? t1 - 1 : max(t1 - 1, g.T - 1 - t0);
+        unsigned int seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.progress + s_need) : "memory");
+        } while (seen < g.ncta);
+        ptx::fence_proxy_async_global();  // generic-proxy y stores -> TMA reads
+        const CUtensorMap* tb = d == 0 ? &tmB0 : &tmB1;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int gi = j * nkb + kb, st = gi % ST;
+          if (gi >= ST) ptx::mbar_wait(&sm.empty[st], ((gi / ST) - 1) & 1);
+          const int pass = kb / nk, kk = kb % nk;
+          const int pa = pass == 2 ? 1 : 0, pb = pass == 1 ? 1 : 0;
+          ptx::mbar_arrive_expect_tx(&sm.full[st], (GBM + BN) * GBK * 2);
+          ptx::tma_load_3d(sm.a[st], &tmA, &sm.full[st], kk * GBK, m0, pa);
+          ptx::tma_load_3d(sm.b[st], tb, &sm.full[st], kk * GBK, n0, pb);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (ptx::elect_one()) {
+      const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
+      for (int j = 0;; ++j) {
+        if (next_tile(j) < 0) break;
+        const int buf = j & 1;
+        if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int gi = j * nkb + kb, st = gi % ST;
+          ptx::mbar_wait(&sm.full[st], (gi / ST) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k) {
+            const uint64_t ad = ptx::sdesc_k_sw128(sm.a[st] + k * 16);
+            const uint64_t bd = ptx::sdesc_k_sw128(sm.b[st] + k * 16);
+            ptx::mma_bf16_ss(acc, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&sm.empty[st]);
+        }
+        ptx::mma_commit(&sm.tmem_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    for (int j = 0;; ++j) {
+      const int t = next_tile(j);
+      if (t < 0) break;
+      const int mt = t / per_m, d = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
+      const int m0 = mt * GBM;
+      const float* __restrict__ bias = g.bias[d];
+      float* __restrict__ C = g.C[d];
+      const int buf = j & 1;
+      ptx::mbar_wait(&sm.tmem_full[buf], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int row = m0 + sub * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(buf * BN + c * 32), v);
+        if (row < g.M) {
+          const int n = n0 + c * 32;
+          float* dst = C + (size_t)row * g.N + n;
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias + n + q);
+            *reinterpret_cast<float4*>(dst + q) =
+                make_float4(v[q] + bb.x, v[q + 1] + bb.y, v[q + 2] + bb.z, v[q + 3] + bb.w);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&sm.tmem_empty[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // fp32 [rows, cols] (row stride ld) -> bf16 planes [2][rows][cols]; the lo
 // plane starts `pstride` elements after the hi plane (pstride = 0: rows*cols)
 __global__ void split_planes_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, size_t rows, int cols,

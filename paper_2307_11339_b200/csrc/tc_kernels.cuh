@@ -104,7 +104,7 @@ __global__ void fill_ones_kernel(float* p, int n) {
 }
 
 struct TcWs {
-  size_t xpl, hbuf, counters, trace, progress, total;
+  size_t xpl, hbuf, counters, trace, progress, claim, total;
 };
 inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   (void)G;
@@ -116,6 +116,7 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   w.counters = off; off += 128 * 128;  // <= 128 chunk counters, one 128-B line each
   w.trace = off;    off += (size_t)160 * kTraceSteps * 16 * 8;
   w.progress = off; off += ((size_t)T * 4 + 255) / 256 * 256;  // per-step output counters (host-buffer forward)
+  w.claim = off;    off += 256;                                     // tile claim counter of the overlapped K1
   w.total = off;
   return w;
 }
@@ -295,6 +296,30 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("gemm_xproj_kernel launch: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  ++g_launch_count;
+  return 0;
+}
+
+// Overlapped K1 of the next layer (gemm_xproj_dyn): one CTA per SM on stream
+// s, launched once the recurrence is resident; *claim must be zeroed before.
+inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
+                           const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
+  CUtensorMap ta, tb0, tb1;
+  int rc = make_map3(&ta, apl, ga.K, ga.M, 2, GBM, err, a_pstride);
+  if (!rc) rc = make_map3(&tb0, wpl[0], ga.K, ga.N, 2, 256, err);
+  if (!rc) rc = make_map3(&tb1, wpl[ga.D > 1 ? 1 : 0], ga.K, ga.N, 2, 256, err);
+  if (rc) return rc;
+  static bool init = false;
+  if (!init) {
+    if ((rc = set_smem(gemm_xproj_dyn, gemm_d_smem_bytes(), err))) return rc;
+    init = true;
+  }
+  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(ta, tb0, tb1, ga);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("gemm_xproj_dyn launch: ") + cudaGetErrorString(e);
     return 2;
   }
   ++g_launch_count;

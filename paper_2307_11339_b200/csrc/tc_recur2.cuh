@@ -322,6 +322,12 @@ __global__ void __launch_bounds__(256, 1)
     if (!last) {
       ptx::fence_proxy_async_global();
       group_release(my_counter);
+      // the group barrier inside group_release also ordered the group's y stores
+      // of step s-1: publish them for the overlapped K1 / device->host copy from
+      // a thread off the critical path (warp 3 of the group: neither the
+      // producer nor the MMA warp), without a barrier or fence of its own
+      if (a.progress && s > 0 && eg == 96)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s - 1) : "memory");
     }
     if (threadIdx.x == 0) HS_TRACE(10);
     // 3. off the critical path: outputs, final state, next step's XP
@@ -343,9 +349,12 @@ __global__ void __launch_bounds__(256, 1)
         if (G == 4) a.cn[d][(size_t)(brow0 + b) * H + unit] = c_reg[k];
       }
     }
-    if (a.progress) {  // y of step s in memory: one increment per group per CTA
+    if (a.progress && last) {  // y of the last two steps in memory: one increment each per group per CTA
       ptx::named_bar(1 + grp, 128);
-      if (eg == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s) : "memory");
+      if (eg == 96) {
+        if (s > 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s - 1) : "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s) : "memory");
+      }
     }
     if (!last) load_xproj(s + 1);
   }
