@@ -367,8 +367,60 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   for (int i = 0; i < nev; ++i) HS_CUDA(cudaEventCreate(&evs[i]));
   if (nev) HS_CUDA(cudaEventRecord(evs[0], s));
   int rc;
+  // Layer overlap: layer l+1's input projection (K1) runs on a second stream
+  // while layer l's recurrence is still running (gemm_xproj_dyn, in-kernel
+  // progress waits) — on the SMs the persistent recurrence leaves free, then on
+  // all of them — into the other xproj buffer.
+  static const char* ovl_env = getenv("HS_LAYER_OVERLAP");
+  // batches too large for one co-resident recurrence run as equal slices,
+  // one persistent launch each (no progress counters then)
+  const int Bs = batch_slice(m.G, m.H, m.B, m.D, NPL);
+  if (!Bs) return fail(HS_ERR_UNSUPPORTED, "no tensor-core recurrence plan for B=%d", m.B);
+  const int nsl = (m.B + Bs - 1) / Bs;
+  const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
+  cudaStream_t gs = nullptr;
+  if (overlap && (rc = gemm_stream(&gs))) return rc;
+  // Request overlap (host-buffer forwards, x uploaded in one chunk): this
+  // request's layer-0 split + K1 run on the K1 stream, which the previous
+  // request left gated on its last recurrence being resident — so they fill
+  // the SMs that recurrence leaves free, then all SMs once it exits.  Needs an
+  // even layer count (layer 0 and the last layer use different xproj buffers).
+  static const char* xreq_env = getenv("HS_REQ_OVERLAP");
+  const bool xreq_ok = overlap && m.L % 2 == 0 && gemm_bn(m.G * m.H) == 256 && !(xreq_env && atoi(xreq_env) == 0);
   const bool chunked_in = ov && ov->x_host;
-  if (chunked_in) {
+  if (chunked_in && xreq_ok && (m.T < m.upload_chunks ? m.T : m.upload_chunks) == 1) {
+    cudaEvent_t x_free;
+    bool seen;
+    if ((rc = x_free_event(x, &x_free, &seen))) return rc;
+    if (seen) {
+      HS_CUDA(cudaStreamWaitEvent(ov->cs_in, x_free, 0));  // previous forward done reading this buffer
+    } else if ((rc = join(s, ov->cs_in))) {
+      return rc;
+    }
+    HS_CUDA(cudaMemcpyAsync(const_cast<float*>(x), ov->x_host, TB * m.I * sizeof(float), cudaMemcpyHostToDevice,
+                            ov->cs_in));
+    // gs order already puts this after the previous forward's last K1 (xpl and
+    // this xproj buffer are free then); it must NOT wait for s, which is still
+    // running the previous forward's last recurrence
+    if ((rc = join(ov->cs_in, gs))) return rc;
+    if ((rc = split_planes(x, xpl, TB, m.I, gs, g_err, TB * m.I))) return rc;
+    HS_CUDA(cudaEventRecord(x_free, gs));  // x consumed: the next upload into it may start
+    unsigned int* claim = reinterpret_cast<unsigned int*>(tcws + tw.claim);
+    HS_CUDA(cudaMemsetAsync(claim, 0, sizeof(unsigned int), gs));
+    GemmDynArgs ga{};
+    const __nv_bfloat16* wpl[2] = {nullptr, nullptr};
+    for (int d = 0; d < m.D; ++d) {
+      wpl[d] = at<__nv_bfloat16>(packed, pl.ld[d].tc);
+      ga.bias[d] = at<float>(packed, pl.ld[d].bias_x);
+      ga.C[d] = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
+    }
+    ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.I; ga.npass = NPL == 2 ? 3 : 1;
+    ga.D = m.D; ga.T = m.T; ga.B = m.B;
+    ga.claim = claim;
+    ga.progress = nullptr;  // rows are all present
+    if ((rc = gemm_planes_dyn(xpl, TB * m.I, wpl, ga, di.sms, gs, g_err))) return rc;
+    if ((rc = join(gs, s))) return rc;  // layer-0 XP complete before the recurrence
+  } else if (chunked_in) {
     // upload x in time chunks on the copy stream; split + layer-0 K1 per chunk
     // chunked upload: each chunk's split + K1 starts when it lands (measured
     // c2 stream: 16 chunks 2.37, 4: 2.08, 1: 2.02 ms/request — small chunk
@@ -412,19 +464,6 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
   }
-  // Layer overlap: layer l+1's input projection (K1) runs on a second stream,
-  // one time chunk at a time, as soon as layer l's recurrence has published
-  // that chunk (per-step progress counters + cuStreamWaitValue32) — on the
-  // SMs the persistent recurrence leaves free — into the other xproj buffer.
-  static const char* ovl_env = getenv("HS_LAYER_OVERLAP");
-  // batches too large for one co-resident recurrence run as equal slices,
-  // one persistent launch each (no progress counters then)
-  const int Bs = batch_slice(m.G, m.H, m.B, m.D, NPL);
-  if (!Bs) return fail(HS_ERR_UNSUPPORTED, "no tensor-core recurrence plan for B=%d", m.B);
-  const int nsl = (m.B + Bs - 1) / Bs;
-  const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
-  cudaStream_t gs = nullptr;
-  if (overlap && (rc = gemm_stream(&gs))) return rc;
   float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
   for (int l = 0; l < m.L; ++l) {
     const int Il = m.in_size(l);
@@ -469,7 +508,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
       // counters zeroed before the copy / K1 stream polls them
       if (drain && (rc = join(s, ov->cs_out))) return rc;
-      if (feed_next && (rc = join(s, gs))) return rc;
+      if ((feed_next || (drain && xreq_ok)) && (rc = join(s, gs))) return rc;
     }
     static const bool dbg = getenv("HS_DEBUG_HOSTIO") != nullptr;
     cudaEvent_t dbg_ev[12];
@@ -571,6 +610,10 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);  // two-group: one increment per group
       WaitValue32Fn wait = nsl == 1 ? wait_value_fn() : nullptr;
       if (!wait && (rc = join(s, ov->cs_out))) return rc;  // no stream memory ops / sliced: drain after the kernel
+      if (wait && xreq_ok) {  // gate the next request's layer-0 K1 on this recurrence being resident
+        CUresult r = wait(gs, reinterpret_cast<CUdeviceptr>(a.progress), ncta, 0 /*GEQ*/);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      }
       const int nco = m.T < 16 ? m.T : 16;
       const size_t row = (size_t)m.B * m.D * m.H;
       for (int k = 0; k < nco; ++k) {

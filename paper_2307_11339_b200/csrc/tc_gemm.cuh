@@ -349,11 +349,13 @@ __global__ void __launch_bounds__(256, 1)
         // recurrence finished step s_need (a backward direction runs T-1 .. 0)
         const int t0 = m0 / g.B, t1 = min(g.T, (m0 + GBM + g.B - 1) / g.B);
         const int s_need = g.D == 1 ? t1 - 1 : max(t1 - 1, g.T - 1 - t0);
-        unsigned int seen;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.progress + s_need) : "memory");
-        } while (seen < g.ncta);
-        ptx::fence_proxy_async_global();  // generic-proxy y stores -> TMA reads
+        if (g.progress) {  // nullptr: every row is already in memory
+          unsigned int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.progress + s_need) : "memory");
+          } while (seen < g.ncta);
+          ptx::fence_proxy_async_global();  // generic-proxy y stores -> TMA reads
+        }
         const CUtensorMap* tb = d == 0 ? &tmB0 : &tmB1;
         for (int kb = 0; kb < nkb; ++kb) {
           const int gi = j * nkb + kb, st = gi % ST;
