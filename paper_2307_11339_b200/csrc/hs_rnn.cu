@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/hs_rnn.h"
@@ -340,6 +342,69 @@ int join(cudaStream_t s1, cudaStream_t s2) {
   return HS_OK;
 }
 
+// XP streaming head controller.  Layer l's K1 runs as a full-GPU head over the
+// first P timesteps, then the recurrence starts and the rest of K1 runs on the
+// SMs the recurrence leaves free while the recurrence polls per-M-tile
+// readiness.  P is chosen per model shape from the previous forward's measured
+// slack (recurrence end - side K1 end): a Newton step on
+//   slack(P) ~= slack(P_prev) + (P - P_prev) * t_side
+// towards a target slack of a few recurrence steps.  HS_XP_HEAD=<steps> pins P.
+struct XpCtl {
+  double P = -1.0;      // head steps (fractional state)
+  int P_used = 0;       // head of the forward whose events are pending
+  bool pending = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // rec start, rec end, side start, side end
+};
+std::mutex g_xp_mu;
+std::map<std::string, XpCtl> g_xp;
+
+int xp_head(const std::string& key, int T, int* P_out) {
+  static const char* pin = getenv("HS_XP_HEAD");
+  if (pin) {
+    const int v = atoi(pin);
+    *P_out = v < 0 ? 0 : v > T ? T : v;
+    return HS_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_xp_mu);
+  XpCtl& c = g_xp[key];
+  if (c.P < 0) c.P = 0.5 * T;
+  if (c.pending && cudaEventQuery(c.ev[1]) == cudaSuccess && cudaEventQuery(c.ev[3]) == cudaSuccess) {
+    float rec = 0.f, side = 0.f, slack = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&rec, c.ev[0], c.ev[1]));
+    HS_CUDA(cudaEventElapsedTime(&side, c.ev[2], c.ev[3]));
+    HS_CUDA(cudaEventElapsedTime(&slack, c.ev[3], c.ev[1]));
+    const int steps_side = T - c.P_used;
+    if (steps_side > 0 && side > 0.f && rec > 0.f) {
+      const double t_side = side / steps_side;           // ms per timestep of side K1
+      const double target = 3.0 * rec / T + 0.005;       // ~3 recurrence steps + 5 us
+      double np = c.P_used + 0.8 * (target - slack) / t_side;
+      if (np < 0) np = 0;
+      if (np > 0.9 * T) np = 0.9 * T;  // keep a side part so the slack stays measurable
+      c.P = np;
+    }
+    c.pending = false;
+  } else if (c.pending && c.P_used >= T) {
+    c.pending = false;
+  }
+  *P_out = (int)(c.P + 0.5);
+  return HS_OK;
+}
+
+// events of one streamed layer per forward: [0] before the recurrence, [1] after
+// it (stream s); [2] / [3] around the side K1 (stream gs)
+int xp_events(const std::string& key, int P_used, cudaEvent_t** evs) {
+  std::lock_guard<std::mutex> lk(g_xp_mu);
+  XpCtl& c = g_xp[key];
+  *evs = nullptr;
+  if (c.pending) return HS_OK;
+  for (auto& e : c.ev)
+    if (!e) HS_CUDA(cudaEventCreate(&e));
+  c.pending = true;
+  c.P_used = P_used;
+  *evs = c.ev;
+  return HS_OK;
+}
+
 inline void chunk_bounds(int T, int n, int k, int* t0, int* t1) {
   *t0 = (int)((long)T * k / n);
   *t1 = (int)((long)T * (k + 1) / n);
@@ -465,9 +530,35 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     if (rc) return rc;
   }
   float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
+  // XP streaming: each layer's K1 = full-GPU head over the first P timesteps,
+  // then the recurrence (polling per-M-tile readiness) with the rest of K1 on
+  // the SMs it leaves free (replaces the next-layer K1 overlap)
+  static const char* xs_env = getenv("HS_XP_STREAM");
+  // Device-resident forwards only: in host-buffer request streams the SMs the
+  // last recurrence leaves free already carry the next request's layer-0 K1
+  // (request overlap), which a side K1 of the last layer would crowd out.
+  // Worth it only when a layer's K1 is heavy (c2: 206 GFLOP executed per layer,
+  // +5%); for light K1s (c3: 39 GFLOP) the extra launches and polls cost more.
+  const double k1_flop = (NPL == 2 ? 3.0 : 1.0) * 2.0 * (double)TB * m.G * m.H * (double)(m.D * m.H);
+  const bool xstream = overlap && !chunked_in && gemm_bn(m.G * m.H) == 256 &&
+                       (xs_env ? atoi(xs_env) == 1 : k1_flop >= 100e9);
+  char xp_key[160];
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    snprintf(xp_key, sizeof xp_key, "%d:%d:%d:%d:%d:%d:%d:%d:%d", dev, m.G, m.H, m.B, m.T, m.D, m.I, m.L, NPL);
+  }
+  unsigned int* claimv = reinterpret_cast<unsigned int*>(tcws + tw.claim);
+  unsigned int* xready = reinterpret_cast<unsigned int*>(tcws + tw.xready);
   for (int l = 0; l < m.L; ++l) {
     const int Il = m.in_size(l);
     float* xpl_l = xpb[overlap ? (l & 1) : 0];
+    // streamed only where the recurrence's in-place ypl writes (row t, after its
+    // M-tile's K1 tiles are stored) line up with the K1 input rows: Il == D*H
+    const bool xs_layer = xstream && !(chunked_in && l == 0) && Il == m.D * m.H;
+    // this layer's K1 as one launch on s before the recurrence: not streamed and
+    // not already computed (host-upload chunks for layer 0, next-layer overlap)
+    const bool k1_now = !(chunked_in && l == 0) && !xs_layer && !(overlap && !xstream && l > 0);
     if (overlap && l > 0 && (rc = join(gs, s))) return rc;  // layer l's K1 chunks done
     TcRecurArgs a{};
     a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D; a.Bst = m.B;
@@ -478,7 +569,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
       whh[d] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
       float* xp = xpl_l + (size_t)d * TB * m.G * m.H;
-      if (!(chunked_in && l == 0) && !(overlap && l > 0)) {
+      if (k1_now) {
         rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
         if (rc) return rc;
       }
@@ -502,7 +593,45 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
     HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
     const bool drain = last && ov && ov->y_host;
-    const bool feed_next = overlap && !last;
+    const bool feed_next = overlap && !last && !xstream;
+    // ---- XP streaming of this layer's K1 (head on s now, side part after the launch)
+    const int tiles_m = (int)((TB + 127) / 128), per_m = m.D * (m.G * m.H / 256), tiles_all = tiles_m * per_m;
+    int PA = 0, P = 0;
+    GemmDynArgs xga{};
+    const __nv_bfloat16* xwpl[2] = {nullptr, nullptr};
+    cudaEvent_t* xevs = nullptr;
+    if (xs_layer) {
+      if ((rc = xp_head(xp_key, m.T, &P))) return rc;
+      const long rows = (long)P * m.B;
+      PA = (int)((rows + 127) / 128) * per_m;
+      if (PA > tiles_all) PA = tiles_all;
+      HS_CUDA(cudaMemsetAsync(xready, 0, (size_t)tiles_m * 4, s));
+      HS_CUDA(cudaMemsetAsync(claimv + 32, 0, 96 * 4, s));  // head / side claim counters + started
+      for (int d = 0; d < m.D; ++d) {
+        const LayerPack& lp = pl.ld[l * m.D + d];
+        xwpl[d] = at<__nv_bfloat16>(packed, lp.tc);
+        xga.bias[d] = at<float>(packed, lp.bias_x);
+        xga.C[d] = xpl_l + (size_t)d * TB * m.G * m.H;
+      }
+      xga.M = (int)TB; xga.N = m.G * m.H; xga.K = Il; xga.npass = NPL == 2 ? 3 : 1;
+      xga.D = m.D; xga.T = m.T; xga.B = m.B;
+      xga.xready = xready;
+      if (PA > 0) {
+        GemmDynArgs ha = xga;
+        ha.claim = claimv + 32;
+        ha.tile_begin = 0;
+        ha.tile_end = PA;
+        if ((rc = gemm_planes_dyn(xpl, TB * Il, xwpl, ha, di.sms, s, g_err))) return rc;
+      }
+      if (PA < tiles_all) {
+        a.xready = xready;
+        a.xready_target = (unsigned int)per_m;
+        a.started = claimv + 96;
+        if ((rc = join(s, gs))) return rc;  // the side launch sees the zeroed counters
+        if ((rc = xp_events(xp_key, P, &xevs))) return rc;
+        if (xevs) HS_CUDA(cudaEventRecord(xevs[0], s));
+      }
+    }
     if (drain || feed_next) {
       a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);
       HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
@@ -530,7 +659,24 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     } else if (nsl == 1) {
       rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
       if (rc) return rc;
-    } else {
+    }
+    if (xs_layer && PA < tiles_all) {
+      // side part of this layer's K1: once every recurrence CTA is resident,
+      // on the SMs it leaves free (one CTA each; the recurrence polls xready)
+      const unsigned int rec_ctas = (unsigned int)(a.D * a.RB * a.S);
+      if (xevs) HS_CUDA(cudaEventRecord(xevs[1], s));
+      CUresult r = wait_value_fn()(gs, reinterpret_cast<CUdeviceptr>(a.started), rec_ctas, 0 /*GEQ*/);
+      if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      if (xevs) HS_CUDA(cudaEventRecord(xevs[2], gs));
+      GemmDynArgs sa = xga;
+      sa.claim = claimv + 64;
+      sa.tile_begin = PA;
+      sa.tile_end = tiles_all;
+      const int side = di.sms - (int)rec_ctas;
+      if ((rc = gemm_planes_dyn(xpl, TB * Il, xwpl, sa, side > 0 ? side : 1, gs, g_err))) return rc;
+      if (xevs) HS_CUDA(cudaEventRecord(xevs[3], gs));
+    }
+    if (nsl > 1) {
       for (int j = 0; j < nsl; ++j) {
         const int b0 = j * Bs, bn = m.B - b0 < Bs ? m.B - b0 : Bs;
         TcRecurArgs sa = a;

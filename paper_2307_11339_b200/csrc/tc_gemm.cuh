@@ -280,6 +280,8 @@ struct GemmDynArgs {
   unsigned int* claim;             // zeroed before launch
   const unsigned int* progress;    // [T] CTAs of the recurrence that finished step s
   unsigned int ncta;               // progress[s] value meaning "step s complete everywhere"
+  int tile_begin, tile_end;        // claimable tile range (tile_end <= 0: all)
+  unsigned int* xready;            // optional [M-tiles]: +1 per stored tile (XP streaming into a running recurrence)
 };
 
 struct GemmDSmem {
@@ -306,7 +308,8 @@ __global__ void __launch_bounds__(256, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = g.K / GBK, nkb = g.npass * nk;
   const int tiles_n = g.N / BN, per_m = g.D * tiles_n;
-  const int tiles = ((g.M + GBM - 1) / GBM) * per_m;
+  const int tiles_all = ((g.M + GBM - 1) / GBM) * per_m;
+  const int tiles = g.tile_end > 0 && g.tile_end < tiles_all ? g.tile_end : tiles_all;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (ptx::elect_one()) {
       for (int j = 0;; ++j) {
-        int t = (int)atomicAdd(g.claim, 1u);
+        int t = g.tile_begin + (int)atomicAdd(g.claim, 1u);
         if (t >= tiles) t = -1;
         sm.tq[j % NQ] = t;
         ptx::mbar_arrive(&sm.tq_full[j % NQ]);
@@ -425,6 +428,11 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&sm.tmem_empty[buf]);
+      if (g.xready) {  // the 4 epilogue warps' stores of this tile -> one release
+        ptx::named_bar(1, 128);
+        if (warp == 4 && lane == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.xready + mt) : "memory");
+      }
     }
   }
   ptx::tc_fence_before();

@@ -104,7 +104,7 @@ __global__ void fill_ones_kernel(float* p, int n) {
 }
 
 struct TcWs {
-  size_t xpl, hbuf, counters, trace, progress, claim, total;
+  size_t xpl, hbuf, counters, trace, progress, claim, xready, total;
 };
 inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   (void)G;
@@ -116,7 +116,8 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   w.counters = off; off += 128 * 128;  // <= 128 chunk counters, one 128-B line each
   w.trace = off;    off += (size_t)160 * kTraceSteps * 16 * 8;
   w.progress = off; off += ((size_t)T * 4 + 255) / 256 * 256;  // per-step output counters (host-buffer forward)
-  w.claim = off;    off += 256;                                     // tile claim counter of the overlapped K1
+  w.claim = off;    off += 512;  // tile claim counters of the dynamic K1 launches ([0], [32], [64]) + started ([96])
+  w.xready = off;   off += (((size_t)T * B + 127) / 128 * 4 + 255) / 256 * 256;  // per-M-tile XP readiness
   w.total = off;
   return w;
 }

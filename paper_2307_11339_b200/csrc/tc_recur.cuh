@@ -47,7 +47,32 @@ struct TcRecurArgs {
   unsigned long long* trace;    // optional [grid][kTraceSteps][16] %globaltimer stamps (debug)
   unsigned int* progress;       // optional [T]: progress[s] counts CTAs whose outputs of step s are in memory
   unsigned int group_offset_ns; // two-group kernel: initial phase offset of group 1 (0 = none)
+  // XP streaming (K1 of this layer still running): xready[m] counts the K1
+  // tiles of M-tile m (rows [128m, 128m+128) of xproj) already stored;
+  // timestep t may be read once its M-tiles reach xready_target.  nullptr = all present.
+  const unsigned int* xready;
+  unsigned int xready_target;
+  unsigned int* started;        // optional: +1 per CTA once resident (gates the side-stream K1)
 };
+
+// Block until the K1 tiles holding timestep tt's rows of xproj are stored.
+// In the time loop ONE lane of an epilogue-only warp does this for step s+1
+// while step s waits for its partial sums; the group / CTA barrier before the
+// h release then orders every thread's XP prefetch after that acquire, so
+// neither the producer nor the MMA warp ever waits on it.
+__device__ __forceinline__ void wait_xready(const TcRecurArgs& a, int tt) {
+  if (!a.xready) return;
+  const int lo = (tt * a.Bst) / 128, hi = (tt * a.Bst + a.Bst - 1) / 128;
+  for (int mt = lo; mt <= hi; ++mt) {
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.xready + mt) : "memory");
+    } while (v < a.xready_target);
+  }
+}
+__device__ __forceinline__ void signal_started(const TcRecurArgs& a) {
+  if (a.started && threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.started) : "memory");
+}
 
 constexpr int kTraceSteps = 64;
 
@@ -136,6 +161,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 atoms need 1024-B alignment
+  signal_started(a);
   const int H = a.H, B = a.B, Npad = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
   const RecurLayout L = recur_layout(G, H, Npad, S, NPL, NSW);
   const int nch = L.nch;
@@ -237,14 +263,15 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
     bias_z = a.bias_h[d][H + unit];
     bias_n = a.bias_h[d][2 * H + unit];
   }
-  auto load_xproj = [&](int step) {
+  auto load_xproj = [&](int step, bool poll) {
     const int tt = d == 0 ? step : T - 1 - step;
+    if (poll) wait_xready(a, tt);
     const float* __restrict__ xp = a.xproj[d] + (size_t)tt * a.Bst * GH + unit;
 #pragma unroll
     for (int k = 0; k < CELLS; ++k) {
       const int b = b0 + k * bstep;
 #pragma unroll
-      for (int g = 0; g < G; ++g) xq[k][g] = b < B ? __ldg(xp + (size_t)b * GH + g * H) : 0.f;
+      for (int g = 0; g < G; ++g) xq[k][g] = b < B ? __ldcg(xp + (size_t)b * GH + g * H) : 0.f;  // may be written by a running K1
     }
   };
 #pragma unroll
@@ -259,7 +286,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
     }
   }
   ptx::fence_proxy_async_global();
-  load_xproj(0);
+  load_xproj(0, true);
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
   cluster_arrive();  // every CTA's barriers initialised before any remote op
@@ -372,6 +399,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
       }
     }
     if (e == 128) HS_TRACE(4);
+    if (e == kEpiThreads - 32 && !last) wait_xready(a, d == 0 ? s + 1 : T - 2 - s);  // next step's XP (see wait_xready)
     ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units are in my shared memory
     if (e == 0 && !last)  // next phase: the peers' bulk copies of step s+1
       ptx::mbar_arrive_expect_tx(red_full, (uint32_t)((S - 1) * region_floats * 4));
@@ -442,7 +470,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
         if (G == 4) a.cn[d][(size_t)b * H + unit] = c_reg[k];
       }
     }
-    if (!last) load_xproj(s + 1);
+    if (!last) load_xproj(s + 1, false);  // ordered after warp 7's wait_xready by the barrier above
     if (e == 0) HS_TRACE(11);
   }
   cluster_arrive();  // no CTA leaves while peers may still copy into it / arrive on its barriers

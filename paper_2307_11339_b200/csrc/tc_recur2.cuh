@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem_raw) & 1023) __trap();
+  signal_started(a);
   // a.B = total batch, a.Npad = padded rows of one group (Bh = ceil(B/2) rows each)
   const int H = a.H, B = a.B, Np = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
   const int Bh = (B + 1) / 2;
@@ -152,14 +153,15 @@ __global__ void __launch_bounds__(256, 1)
     bias_z = a.bias_h[d][H + unit];
     bias_n = a.bias_h[d][2 * H + unit];
   }
-  auto load_xproj = [&](int step) {
+  auto load_xproj = [&](int step, bool poll) {
     const int tt = d == 0 ? step : T - 1 - step;
+    if (poll) wait_xready(a, tt);
     const float* __restrict__ xp = a.xproj[d] + (size_t)tt * a.Bst * GH + unit;
 #pragma unroll
     for (int k = 0; k < CELLS; ++k) {
       const int b = b0 + k * bstep;
 #pragma unroll
-      for (int g = 0; g < G; ++g) xq[k][g] = b < Bg ? __ldg(xp + (size_t)(brow0 + b) * GH + g * H) : 0.f;
+      for (int g = 0; g < G; ++g) xq[k][g] = b < Bg ? __ldcg(xp + (size_t)(brow0 + b) * GH + g * H) : 0.f;
     }
   };
   auto group_release = [&](unsigned int* ctr) {  // the group's 4 warps, then one release
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   ptx::fence_proxy_async_global();
-  load_xproj(0);
+  load_xproj(0, true);
   group_release(my_counter);
   cluster_arrive();  // every CTA's barriers initialised before any remote op
   cluster_wait();
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::bulk_wait_read0();  // staging reusable (next step's drain comes long after)
     }
     if (threadIdx.x == 64) HS_TRACE(4);
+    if (eg == 96 && !last) wait_xready(a, d == 0 ? s + 1 : T - 2 - s);  // next step's XP (see wait_xready)
     ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units landed
     if (threadIdx.x == 64) HS_TRACE(5);
     if (eg == 0 && !last)  // next phase: the peers' bulk copies of step s+1
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(256, 1)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s) : "memory");
       }
     }
-    if (!last) load_xproj(s + 1);
+    if (!last) load_xproj(s + 1, false);  // ordered after warp 3's wait_xready by group_release's barrier
   }
   cluster_arrive();  // no CTA leaves while peers may still write its partials / barriers
   cluster_wait();
