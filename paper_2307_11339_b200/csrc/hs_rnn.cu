@@ -312,6 +312,58 @@ WaitValue32Fn wait_value_fn() {
   return fn;
 }
 
+// One-time probe per device: do two kernels on different streams actually run
+// concurrently here?  Kernel A spins (<= 20 ms of %globaltimer) on a flag that
+// kernel B, launched after it on another stream, sets.  Profilers and
+// sanitizers that serialise launches (and CUDA_LAUNCH_BLOCKING) make A time
+// out.  XP streaming — a recurrence waiting on a K1 launched after it — is only
+// enabled where this holds.
+__global__ void probe_wait_kernel(volatile unsigned int* flag, unsigned int* result) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0u) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000ull) {
+      *result = 2u;
+      return;
+    }
+  }
+  *result = 1u;
+}
+__global__ void probe_set_kernel(volatile unsigned int* flag) { *flag = 1u; }
+
+bool kernels_run_concurrently() {
+  static std::mutex mu;
+  static int cache[16] = {};  // 0 unknown, 1 yes, 2 no
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[dev]) return cache[dev] == 1;
+  cache[dev] = 2;
+  unsigned int* buf = nullptr;
+  cudaStream_t a = nullptr, b = nullptr;
+  unsigned int result = 0;
+  if (cudaMalloc(&buf, 8) == cudaSuccess && cudaMemset(buf, 0, 8) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking) == cudaSuccess) {
+    // load both kernels first: with lazy module loading, loading B at its launch
+    // would wait for the spinning A (the same holds for the side K1 below)
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, probe_wait_kernel);
+    cudaFuncGetAttributes(&fa, probe_set_kernel);
+    probe_wait_kernel<<<1, 1, 0, a>>>(buf, buf + 1);
+    probe_set_kernel<<<1, 1, 0, b>>>(buf);
+    if (cudaStreamSynchronize(a) == cudaSuccess && cudaStreamSynchronize(b) == cudaSuccess &&
+        cudaMemcpy(&result, buf + 1, 4, cudaMemcpyDeviceToHost) == cudaSuccess && result == 1u)
+      cache[dev] = 1;
+  }
+  if (a) cudaStreamDestroy(a);
+  if (b) cudaStreamDestroy(b);
+  if (buf) cudaFree(buf);
+  cudaGetLastError();
+  return cache[dev] == 1;
+}
+
 int gemm_stream(cudaStream_t* out) {
   static thread_local cudaStream_t cache[16] = {};
   int dev;
@@ -540,8 +592,12 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   // Worth it only when a layer's K1 is heavy (c2: 206 GFLOP executed per layer,
   // +5%); for light K1s (c3: 39 GFLOP) the extra launches and polls cost more.
   const double k1_flop = (NPL == 2 ? 3.0 : 1.0) * 2.0 * (double)TB * m.G * m.H * (double)(m.D * m.H);
+  // The recurrence waits on a kernel launched after it, so this relies on the
+  // two running concurrently: off where launches are serialised (profilers,
+  // sanitizers, CUDA_LAUNCH_BLOCKING: kernels_run_concurrently) and, per layer
+  // below, unless >= 16 SMs stay free beside the recurrence.
   const bool xstream = overlap && !chunked_in && gemm_bn(m.G * m.H) == 256 &&
-                       (xs_env ? atoi(xs_env) == 1 : k1_flop >= 100e9);
+                       (xs_env ? atoi(xs_env) == 1 : k1_flop >= 100e9) && kernels_run_concurrently();
   char xp_key[160];
   {
     int dev = 0;
@@ -594,13 +650,32 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
     const bool drain = last && ov && ov->y_host;
     const bool feed_next = overlap && !last && !xstream;
+    // two batch-half groups per CTA (tc_recur2.cuh) when the batch is large
+    // enough for both chains to carry work: c2 (B=64) 6.85 -> 6.58 us/step;
+    // slower at B=32 (c3: 4.25 -> 4.68 ms).  HS_TWO_GROUPS=0/1 overrides.
+    static const char* two_env = getenv("HS_TWO_GROUPS");
+    const bool two_req = two_env ? atoi(two_env) == 1 : m.B >= 64;
+    const bool two = nsl == 1 && two_req && choose_split2(m.G, m.H, m.B, m.D, NPL) > 0;
     // ---- XP streaming of this layer's K1 (head on s now, side part after the launch)
     const int tiles_m = (int)((TB + 127) / 128), per_m = m.D * (m.G * m.H / 256), tiles_all = tiles_m * per_m;
     int PA = 0, P = 0;
     GemmDynArgs xga{};
     const __nv_bfloat16* xwpl[2] = {nullptr, nullptr};
     cudaEvent_t* xevs = nullptr;
-    if (xs_layer) {
+    const bool xs_now = xs_layer && di.sms - recurrence_ctas(m.G, NPL, a, two) >= 16;
+    if (!xs_now && xs_layer) {  // not enough free SMs: the whole K1 before the recurrence
+      for (int d = 0; d < m.D; ++d) {
+        const LayerPack& lp = pl.ld[l * m.D + d];
+        rc = gemm_planes(xpl, at<__nv_bfloat16>(packed, lp.tc), at<float>(packed, lp.bias_x), const_cast<float*>(a.xproj[d]),
+                         (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
+        if (rc) return rc;
+      }
+    }
+    if (xs_now) {
+      // the side K1 is launched while the recurrence already spins on its
+      // output: make sure its module is loaded now (lazy loading would
+      // otherwise wait for the running recurrence)
+      if ((rc = gemm_dyn_preload(g_err))) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
       if ((rc = xp_head(xp_key, m.T, &P))) return rc;
       const long rows = (long)P * m.B;
       PA = (int)((rows + 127) / 128) * per_m;
@@ -645,12 +720,6 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       for (int i = 0; i < 12; ++i) HS_CUDA(cudaEventCreate(&dbg_ev[i]));
       HS_CUDA(cudaEventRecord(dbg_ev[0], s));
     }
-    // two batch-half groups per CTA (tc_recur2.cuh) when the batch is large
-    // enough for both chains to carry work: c2 (B=64) 6.85 -> 6.58 us/step;
-    // slower at B=32 (c3: 4.25 -> 4.68 ms).  HS_TWO_GROUPS=0/1 overrides.
-    static const char* two_env = getenv("HS_TWO_GROUPS");
-    const bool two_req = two_env ? atoi(two_env) == 1 : m.B >= 64;
-    const bool two = nsl == 1 && two_req && choose_split2(m.G, m.H, m.B, m.D, NPL) > 0;
     if (two) {
       static const char* off_env = getenv("HS_TG_OFFSET_NS");
       a.group_offset_ns = off_env ? (unsigned int)atoi(off_env) : 0u;
@@ -660,7 +729,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
       if (rc) return rc;
     }
-    if (xs_layer && PA < tiles_all) {
+    if (xs_now && PA < tiles_all) {
       // side part of this layer's K1: once every recurrence CTA is resident,
       // on the SMs it leaves free (one CTA each; the recurrence polls xready)
       const unsigned int rec_ctas = (unsigned int)(a.D * a.RB * a.S);

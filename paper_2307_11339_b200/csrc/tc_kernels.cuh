@@ -305,6 +305,16 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
 
 // Overlapped K1 of the next layer (gemm_xproj_dyn): one CTA per SM on stream
 // s, launched once the recurrence is resident; *claim must be zeroed before.
+inline int gemm_dyn_preload(std::string& err) {  // loads the module (lazy loading) + smem opt-in, once
+  static bool init = false;
+  if (!init) {
+    int rc = set_smem(gemm_xproj_dyn, gemm_d_smem_bytes(), err);
+    if (rc) return rc;
+    init = true;
+  }
+  return 0;
+}
+
 inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
                            const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
   CUtensorMap ta, tb0, tb1;
@@ -312,11 +322,7 @@ inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __n
   if (!rc) rc = make_map3(&tb0, wpl[0], ga.K, ga.N, 2, 256, err);
   if (!rc) rc = make_map3(&tb1, wpl[ga.D > 1 ? 1 : 0], ga.K, ga.N, 2, 256, err);
   if (rc) return rc;
-  static bool init = false;
-  if (!init) {
-    if ((rc = set_smem(gemm_xproj_dyn, gemm_d_smem_bytes(), err))) return rc;
-    init = true;
-  }
+  if ((rc = gemm_dyn_preload(err))) return rc;
   gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(ta, tb0, tb1, ga);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -571,6 +577,25 @@ inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, Tc
       return 3;
     }
   }, err);
+}
+
+// CTAs the recurrence launch for this layer will use (same split choice as
+// recurrence_layer / recurrence_layer2), without launching; 0 = infeasible.
+inline int recurrence_ctas(int G, int NPL, const TcRecurArgs& a, bool two) {
+  if (two) {
+    const int S = choose_split2(G, a.H, a.B, a.D, NPL);
+    return S ? a.D * (a.H / 32) * S : 0;
+  }
+  int nsw_try = 0;
+  auto limit = [&](int S_) -> int {
+    return max_coresident_ctas(G, NPL, S_, recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total);
+  };
+  int S = choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
+  if (!S) {
+    nsw_try = kSW;
+    S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);
+  }
+  return S ? a.D * (a.H / 32) * S : 0;
 }
 
 }  // namespace tc

@@ -101,3 +101,41 @@ def test_tc_initial_states_bidirectional():
                           h0.double().numpy(), c0.double().numpy(), dirs=2)
     for g, r in zip((y, hn, cn), ref):
         assert float(np.abs(g.cpu().double().numpy() - r).max()) <= 1e-4
+
+
+XS_SHAPES = [
+    RNNSpec("lstm", 2, 512, 12, 64, input=512, algo="tc"),           # two-group recurrence, layer 0 streamed too
+    RNNSpec("lstm", 3, 256, 10, 48, input=512, dirs=2, algo="tc"),   # single-group, bidirectional (D*H = I)
+    RNNSpec("gru", 2, 256, 9, 20, input=64, algo="tc"),              # layer 0 not streamed (I != D*H), layer 1 is
+    CONFIGS["c2"].with_(seq=40),
+]
+
+
+def test_xp_streaming_forced_matches(tmp_path):
+    """XP streaming (the recurrence polls per-M-tile readiness while the rest of
+    its K1 runs beside it) forced on with HS_XP_STREAM=1 in a subprocess: outputs
+    bit-identical to the default schedule and within 1e-4 of the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    out = tmp_path / "xs.pt"
+    code = (
+        "import torch, sys; sys.path.insert(0, '.');"
+        "from paper_2307_11339_b200 import RNNExecutor, RNNSpec, init_weights, make_input;"
+        f"XS_SHAPES = [{', '.join(repr(s) for s in XS_SHAPES)}];"
+        "res = [];"
+        "[res.append([t.cpu() if t is not None else None for t in RNNExecutor(s, init_weights(s, 0)).forward(make_input(s, 1).cuda())]) for s in XS_SHAPES for _ in range(2)];"
+        f"torch.save(res, {str(out)!r})"
+    )
+    env = dict(os.environ, HS_XP_STREAM="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], env=env, cwd=root, check=True, timeout=600)
+    got = torch.load(out)
+    for i, spec in enumerate(XS_SHAPES):
+        w = init_weights(spec, 0)
+        ref = [t.cpu() if t is not None else None for t in RNNExecutor(spec, w).forward(make_input(spec, 1).cuda())]
+        for rep in range(2):
+            for g, r in zip(got[2 * i + rep], ref):
+                assert (g is None and r is None) or torch.equal(g, r), spec
+        assert run(spec) <= 1e-4
