@@ -340,6 +340,9 @@ bool kernels_run_concurrently() {
   std::lock_guard<std::mutex> lk(mu);
   if (cache[dev]) return cache[dev] == 1;
   cache[dev] = 2;
+  // Nsight Compute with a kernel filter (-k) runs the probe unprofiled and
+  // concurrently but serialises the profiled recurrence: detect its injection
+  if (getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR")) return false;
   unsigned int* buf = nullptr;
   cudaStream_t a = nullptr, b = nullptr;
   unsigned int result = 0;
