@@ -400,12 +400,16 @@ int join(cudaStream_t s1, cudaStream_t s2) {
 // XP streaming head controller.  Layer l's K1 runs as a full-GPU head over the
 // first P timesteps, then the recurrence starts and the rest of K1 runs on the
 // SMs the recurrence leaves free while the recurrence polls per-M-tile
-// readiness.  P is chosen per model shape from the previous forward's measured
-// slack (recurrence end - side K1 end): a Newton step on
-//   slack(P) ~= slack(P_prev) + (P - P_prev) * t_side
-// towards a target slack of a few recurrence steps.  HS_XP_HEAD=<steps> pins P.
+// readiness.  The side part must finish a few recurrence steps before an
+// unstalled recurrence would end:
+//   (T - P) * t_side <= T * t_rec - margin
+// t_side (ms per timestep of side K1) is measured on the previous forward; t_rec
+// is the fastest recurrence step seen for this shape (a stalled recurrence only
+// looks slower, so the minimum is the unstalled rate; the first forward runs
+// with P = T/2).  HS_XP_HEAD=<steps> pins P.
 struct XpCtl {
-  double P = -1.0;      // head steps (fractional state)
+  double P = -1.0;      // head steps
+  double rec_min = 1e30;  // fastest recurrence ms per step seen
   int P_used = 0;       // head of the forward whose events are pending
   bool pending = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // rec start, rec end, side start, side end
@@ -429,12 +433,20 @@ int xp_head(const std::string& key, int T, int* P_out) {
     HS_CUDA(cudaEventElapsedTime(&side, c.ev[2], c.ev[3]));
     HS_CUDA(cudaEventElapsedTime(&slack, c.ev[3], c.ev[1]));
     const int steps_side = T - c.P_used;
+    (void)slack;
     if (steps_side > 0 && side > 0.f && rec > 0.f) {
-      const double t_side = side / steps_side;           // ms per timestep of side K1
-      const double target = 3.0 * rec / T + 0.005;       // ~3 recurrence steps + 5 us
-      double np = c.P_used + 0.8 * (target - slack) / t_side;
+      const double t_side = side / steps_side;  // ms per timestep of side K1
+      if (rec / T < c.rec_min) c.rec_min = rec / T;
+      // the side part does not progress evenly: at ~3 steps of slack the
+      // recurrence already stalls (c2: 0.735 -> 0.83 ms), at ~8 it does not
+      const double margin = 8.0 * c.rec_min + 0.010;
+      double np = T - (T * c.rec_min - margin) / t_side;
       if (np < 0) np = 0;
       if (np > 0.9 * T) np = 0.9 * T;  // keep a side part so the slack stays measurable
+      static const bool dbg = getenv("HS_DEBUG_XP") != nullptr;
+      if (dbg)
+        fprintf(stderr, "xp %s: P_used %d rec %.3f ms side %.3f ms slack %.3f ms t_side %.4f rec_min %.4f -> P %.1f\n",
+                key.c_str(), c.P_used, rec, side, slack, t_side, c.rec_min, np);
       c.P = np;
     }
     c.pending = false;
@@ -682,6 +694,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       if ((rc = xp_head(xp_key, m.T, &P))) return rc;
       const long rows = (long)P * m.B;
       PA = (int)((rows + 127) / 128) * per_m;
+      // the head runs in whole waves of one tile per SM: fill its last wave
+      if (PA > 0) PA = (PA + di.sms - 1) / di.sms * di.sms;
       if (PA > tiles_all) PA = tiles_all;
       HS_CUDA(cudaMemsetAsync(xready, 0, (size_t)tiles_m * 4, s));
       HS_CUDA(cudaMemsetAsync(claimv + 32, 0, 96 * 4, s));  // head / side claim counters + started
@@ -706,7 +720,9 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         a.xready_target = (unsigned int)per_m;
         a.started = claimv + 96;
         if ((rc = join(s, gs))) return rc;  // the side launch sees the zeroed counters
-        if ((rc = xp_events(xp_key, P, &xevs))) return rc;
+        // head as run (whole waves), in timesteps: what the side part did not do
+        const int p_eff = (int)((long)PA / per_m * 128 / m.B);
+        if ((rc = xp_events(xp_key, p_eff < m.T ? p_eff : m.T, &xevs))) return rc;
         if (xevs) HS_CUDA(cudaEventRecord(xevs[0], s));
       }
     }

@@ -17,9 +17,9 @@ spec = hs.CONFIGS[cfg]
 ex = hs.RNNExecutor(spec, hs.init_weights(spec))
 x = hs.make_input(spec).cuda()
 outs = ex.alloc_outputs()
-for _ in range(5):
+for _ in range(10):  # synchronised, so per-shape controllers (XP streaming head) see each forward's events
     ex.forward(x, out=outs)
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
     ex.forward(x, out=outs)
     torch.cuda.synchronize()
