@@ -652,7 +652,6 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       a.hn[d] = hn + (size_t)ld * m.B * m.H;
       a.cn[d] = cn ? cn + (size_t)ld * m.B * m.H : nullptr;
     }
-    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
     const bool last = l == m.L - 1;
     a.y = last ? y : nullptr;
     a.ypl = last ? nullptr : xpl;
@@ -739,6 +738,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       for (int i = 0; i < 12; ++i) HS_CUDA(cudaEventCreate(&dbg_ev[i]));
       HS_CUDA(cudaEventRecord(dbg_ev[0], s));
     }
+    // layer_ms split: K1 (incl. an XP-streaming head and the zeroing) | recurrence
+    if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 1], s));
     if (two) {
       static const char* off_env = getenv("HS_TG_OFFSET_NS");
       a.group_offset_ns = off_env ? (unsigned int)atoi(off_env) : 0u;

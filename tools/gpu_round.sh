@@ -15,3 +15,5 @@ timeout 900 compute-sanitizer --tool racecheck python tools/sanitize_case.py > g
 timeout 900 compute-sanitizer --tool synccheck python tools/sanitize_case.py > gpurun_out/synccheck.log 2>&1
 timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_case.py > gpurun_out/memcheck.log 2>&1
 tail -n 3 gpurun_out/*.log
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b_torchrun.log 2>&1
+tail -n 2 gpurun_out/b_torchrun.log
