@@ -6,6 +6,7 @@
 // recurrent wavefront K2/K3), optional CUDA-event timing for the profiler.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -367,6 +368,19 @@ bool kernels_run_concurrently() {
   return cache[dev] == 1;
 }
 
+// zero up to 6 16-byte-aligned regions in one launch
+struct ZeroList {
+  uint4* p[6];
+  size_t n16[6];
+  int k;
+};
+__global__ void zero_list_kernel(ZeroList z) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < z.k; ++r)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < z.n16[r]; i += stride)
+      z.p[r][i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 int gemm_stream(cudaStream_t* out) {
   static thread_local cudaStream_t cache[16] = {};
   int dev;
@@ -427,11 +441,24 @@ int xp_head(const std::string& key, int T, int* P_out) {
   std::lock_guard<std::mutex> lk(g_xp_mu);
   XpCtl& c = g_xp[key];
   if (c.P < 0) c.P = 0.5 * T;
+  *P_out = (int)(c.P + 0.5);
+  return HS_OK;
+}
+
+// Consume the pending events of an earlier forward, if complete, and update P.
+// Called once the whole forward is enqueued (the host is off the GPU's critical
+// path then; reading events costs ~15 us of host time).
+int xp_update(const std::string& key, int T) {
+  std::lock_guard<std::mutex> lk(g_xp_mu);
+  auto it = g_xp.find(key);
+  if (it == g_xp.end()) return HS_OK;
+  XpCtl& c = it->second;
   if (c.pending && cudaEventQuery(c.ev[1]) == cudaSuccess && cudaEventQuery(c.ev[3]) == cudaSuccess) {
     float rec = 0.f, side = 0.f, slack = 0.f;
     HS_CUDA(cudaEventElapsedTime(&rec, c.ev[0], c.ev[1]));
     HS_CUDA(cudaEventElapsedTime(&side, c.ev[2], c.ev[3]));
-    HS_CUDA(cudaEventElapsedTime(&slack, c.ev[3], c.ev[1]));
+    static const bool dbg_xp = getenv("HS_DEBUG_XP") != nullptr;
+    if (dbg_xp) HS_CUDA(cudaEventElapsedTime(&slack, c.ev[3], c.ev[1]));
     const int steps_side = T - c.P_used;
     (void)slack;
     if (steps_side > 0 && side > 0.f && rec > 0.f) {
@@ -453,7 +480,6 @@ int xp_head(const std::string& key, int T, int* P_out) {
   } else if (c.pending && c.P_used >= T) {
     c.pending = false;
   }
-  *P_out = (int)(c.P + 0.5);
   return HS_OK;
 }
 
@@ -660,8 +686,27 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     static const char* trace_path = getenv("HS_RECUR_TRACE");
     a.trace = trace_path && l == 0 ? reinterpret_cast<unsigned long long*>(tcws + tw.trace) : nullptr;
     if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
-    HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
-    HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
+    // one launch zeroes every per-layer counter / exchange region (h exchange
+    // planes, chunk counters, XP readiness, claim + started counters, per-step
+    // progress) instead of five memsets (~10 us of serial gaps per layer at c2)
+    {
+      ZeroList zl{};
+      auto add = [&](void* p, size_t bytes) {
+        zl.p[zl.k] = reinterpret_cast<uint4*>(p);
+        zl.n16[zl.k++] = (bytes + 15) / 16;
+      };
+      add(hbuf, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2);
+      add(counters, 128 * 128);
+      add(xready, ((TB + 127) / 128) * 4);
+      add(claimv + 32, 96 * 4);
+      add(tcws + tw.progress, (size_t)m.T * 4);
+      zero_list_kernel<<<2 * di.sms, 256, 0, s>>>(zl);
+      HS_CUDA(cudaGetLastError());
+      ++hs::g_launch_count;
+    }
+    static const bool dbg_host = getenv("HS_DEBUG_HOST") != nullptr;  // host-side enqueue latency (us)
+    auto tnow = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double tz = dbg_host ? tnow() : 0.0;
     const bool drain = last && ov && ov->y_host;
     const bool feed_next = overlap && !last && !xstream;
     // two batch-half groups per CTA (tc_recur2.cuh) when the batch is large
@@ -676,7 +721,9 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     GemmDynArgs xga{};
     const __nv_bfloat16* xwpl[2] = {nullptr, nullptr};
     cudaEvent_t* xevs = nullptr;
+    const double th0 = dbg_host ? tnow() : 0.0;
     const bool xs_now = xs_layer && di.sms - recurrence_ctas(m.G, NPL, a, two) >= 16;
+    const double th1 = dbg_host ? tnow() : 0.0;
     if (!xs_now && xs_layer) {  // not enough free SMs: the whole K1 before the recurrence
       for (int d = 0; d < m.D; ++d) {
         const LayerPack& lp = pl.ld[l * m.D + d];
@@ -690,14 +737,14 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       // output: make sure its module is loaded now (lazy loading would
       // otherwise wait for the running recurrence)
       if ((rc = gemm_dyn_preload(g_err))) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+      const double th2 = dbg_host ? tnow() : 0.0;
       if ((rc = xp_head(xp_key, m.T, &P))) return rc;
+      const double th3 = dbg_host ? tnow() : 0.0;
       const long rows = (long)P * m.B;
       PA = (int)((rows + 127) / 128) * per_m;
       // the head runs in whole waves of one tile per SM: fill its last wave
       if (PA > 0) PA = (PA + di.sms - 1) / di.sms * di.sms;
       if (PA > tiles_all) PA = tiles_all;
-      HS_CUDA(cudaMemsetAsync(xready, 0, (size_t)tiles_m * 4, s));
-      HS_CUDA(cudaMemsetAsync(claimv + 32, 0, 96 * 4, s));  // head / side claim counters + started
       for (int d = 0; d < m.D; ++d) {
         const LayerPack& lp = pl.ld[l * m.D + d];
         xwpl[d] = at<__nv_bfloat16>(packed, lp.tc);
@@ -714,6 +761,9 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         ha.tile_end = PA;
         if ((rc = gemm_planes_dyn(xpl, TB * Il, xwpl, ha, di.sms, s, g_err))) return rc;
       }
+      if (dbg_host)
+        fprintf(stderr, "host us: to xs %.1f rec_ctas %.1f preload %.1f xp_head %.1f head launch %.1f\n", th0 - tz,
+                th1 - th0, th2 - th1, th3 - th2, tnow() - th3);
       if (PA < tiles_all) {
         a.xready = xready;
         a.xready_target = (unsigned int)per_m;
@@ -726,8 +776,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       }
     }
     if (drain || feed_next) {
-      a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);
-      HS_CUDA(cudaMemsetAsync(a.progress, 0, (size_t)m.T * 4, s));
+      a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);  // zeroed with the layer's regions above
       // counters zeroed before the copy / K1 stream polls them
       if (drain && (rc = join(s, ov->cs_out))) return rc;
       if ((feed_next || (drain && xreq_ok)) && (rc = join(s, gs))) return rc;
@@ -888,6 +937,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     }
     if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
   }
+  if (xstream && (rc = xp_update(xp_key, m.T))) return rc;  // the GPU has the last layer to run meanwhile
   if (nev) {
     HS_CUDA(cudaEventSynchronize(evs[nev - 1]));
     for (int l = 0; l < m.L; ++l) {

@@ -4,7 +4,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <type_traits>
 
 #include "simt_kernels.cuh"
@@ -228,6 +231,22 @@ inline EncodeTiledFn encode_fn() {
 // planes are `pstride` elements apart (0: inner*rows, i.e. dense).
 inline int make_map3(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t planes, uint32_t box_rows,
                      std::string& err, uint64_t pstride = 0) {
+  // memoised: a forward encodes ~10 maps over the same few buffers every call
+  // (~1-3 us of host time each, on the enqueue path of every layer)
+  struct Entry {
+    const void* base;
+    uint64_t inner, rows, planes, pstride;
+    uint32_t box_rows;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[32];
+  static thread_local int next = 0;
+  for (const Entry& e : cache)
+    if (e.base == base && e.inner == inner && e.rows == rows && e.planes == planes && e.pstride == pstride &&
+        e.box_rows == box_rows && base) {
+      *map = e.map;
+      return 0;
+    }
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     err = "cuTensorMapEncodeTiled unavailable";
@@ -244,6 +263,9 @@ inline int make_map3(CUtensorMap* map, const void* base, uint64_t inner, uint64_
     err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r);
     return 2;
   }
+  Entry& e = cache[next];
+  next = (next + 1) % 32;
+  e = Entry{base, inner, rows, planes, pstride, box_rows, *map};
   return 0;
 }
 
@@ -349,6 +371,33 @@ inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int col
   return 0;
 }
 
+// cudaOccupancyMaxActiveClusters, memoised per (kernel, device, smem, block,
+// cluster): the query costs ~10 us of host time and sits on the launch path of
+// every layer (the first layer's K1 head waited ~36 us for the host at c2)
+template <typename K>
+inline cudaError_t occ_clusters(int* n, K kernel, const cudaLaunchConfig_t& cfg) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, unsigned, unsigned>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, cfg.dynamicSmemBytes, cfg.blockDim.x,
+                                   cfg.attrs[0].val.clusterDim.x);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *n = it->second;
+      return cudaSuccess;
+    }
+  }
+  const cudaError_t e = cudaOccupancyMaxActiveClusters(n, kernel, &cfg);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = *n;
+  }
+  return e;
+}
+
 template <int G, int NPL>
 inline int max_coresident_ctas_t(int S, size_t smem) {
   static bool init = false;
@@ -370,7 +419,7 @@ inline int max_coresident_ctas_t(int S, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, recur_tc_kernel<G, NPL, 1, 0>, &cfg) != cudaSuccess) {
+  if (occ_clusters(&n, recur_tc_kernel<G, NPL, 1, 0>, cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -404,7 +453,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc_kernel<G, NPL, CELLS, NSW>, &cfg);
+  cudaError_t e = occ_clusters(&nclusters, recur_tc_kernel<G, NPL, CELLS, NSW>, cfg);
   if (e != cudaSuccess) {
     err = std::string("cudaOccupancyMaxActiveClusters: ") + cudaGetErrorString(e);
     return 2;
@@ -535,7 +584,7 @@ inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, recur_tc2_kernel<G, NPL, CELLS>, &cfg);
+  cudaError_t e = occ_clusters(&nclusters, recur_tc2_kernel<G, NPL, CELLS>, cfg);
   if (e != cudaSuccess || nclusters * S < (int)cfg.gridDim.x) {
     err = "two-group recurrent kernel cannot be co-resident";
     return 3;
