@@ -403,11 +403,18 @@ int copy_stream(int which, cudaStream_t* out) {
 
 // s2 waits for all work enqueued on s1 so far
 int join(cudaStream_t s1, cudaStream_t s2) {
-  cudaEvent_t ev;
-  HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  // a small per-thread pool: cudaStreamWaitEvent captures the event's state
+  // when it is enqueued, so an event may be re-recorded right after
+  static thread_local cudaEvent_t pool[16][16] = {};  // [device][slot]: events belong to a device
+  static thread_local int next[16] = {};
+  int dev = 0;
+  HS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
+  cudaEvent_t& ev = pool[dev][next[dev]];
+  next[dev] = (next[dev] + 1) % 16;
+  if (!ev) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   HS_CUDA(cudaEventRecord(ev, s1));
   HS_CUDA(cudaStreamWaitEvent(s2, ev, 0));
-  HS_CUDA(cudaEventDestroy(ev));
   return HS_OK;
 }
 
