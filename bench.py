@@ -120,56 +120,91 @@ def spec_name(spec) -> str:
     return "custom"
 
 
-def oracle_forward_sample(spec, weights, x):
-    """One float64 oracle forward (the reference-arm / cpu_baseline unit)."""
-    from oracle.rnn_ref import rnn_forward_ref
-
-    return rnn_forward_ref(spec.cell, x, weights, dirs=spec.dirs)
-
-
-def cpu_sample_setup(spec, sample_batch):
-    from paper_2307_11339_b200 import init_weights, make_input
-
-    w = [{k: v.double().numpy() for k, v in d.items()} for d in init_weights(spec, 0)]
-    x = make_input(spec, 1)[:, :sample_batch].double().numpy().copy()
-    return w, x
+def ref_sample_spec(spec, sample_batch: int, sample_seq: int):
+    """The bounded CPU sample of the workload: the first ``sample_batch``
+    sequences (and, for long configs, the first ``sample_seq`` timesteps)."""
+    return spec.with_(batch=min(spec.batch, sample_batch), seq=min(spec.seq, sample_seq or spec.seq), algo="auto")
 
 
-def time_cpu_baseline(spec, budget_s: float, sample_batch: int):
-    """Oracle port on the host cores, bounded to ~budget_s seconds."""
-    w, x = cpu_sample_setup(spec, sample_batch)
+class HostReference:
+    """BASELINE.md §2 host-CPU path on the sample: fp32 torch, all host
+    threads; (b) cell-by-cell in Plan.order (Chrion-style per-operator
+    dispatch, oracle/rnn_cells_f32.py) is the timed reference, (a) fused
+    torch.nn.LSTM/GRU is reported beside it."""
+
+    def __init__(self, spec, sample_batch: int, sample_seq: int):
+        import torch
+
+        from oracle.rnn_cells_f32 import _Cells, fused_forward_f32, plan_order
+        from paper_2307_11339_b200 import init_weights, make_input
+
+        reference_planner()  # baseline/_ref on sys.path: the reference planner orders the cells
+        self.threads = len(os.sched_getaffinity(0))
+        torch.set_num_threads(self.threads)
+        self.full = spec
+        self.spec = ref_sample_spec(spec, sample_batch, sample_seq)
+        self.weights = init_weights(spec, 0)
+        self.x = make_input(spec, 1)[: self.spec.seq, : self.spec.batch].contiguous()
+        self.order, self.planner_src = plan_order(self.spec)
+        self.cells = _Cells(self.weights)
+        self.fused = fused_forward_f32(self.spec, self.weights)
+        # seqs/s at the FULL sequence length: a T-prefix sample scales by T / sample_seq
+        self.seq_scale = self.spec.seq / spec.seq
+
+    def step(self):
+        from oracle.rnn_cells_f32 import cells_forward_f32
+
+        return cells_forward_f32(self.spec.cell, self.x, None, self.order, dirs=self.spec.dirs, prepared=self.cells)
+
+    def time_fused(self, reps=3):
+        import torch
+
+        with torch.no_grad():
+            self.fused(self.x)
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                self.fused(self.x)
+                ts.append(time.perf_counter() - t0)
+        p50 = statistics.median(ts)
+        return {"value": self.spec.batch * self.seq_scale / p50, "p50_ms": p50 * 1e3, "threads": self.threads,
+                "what": "fused torch.nn.%s fp32 (best-case host path)" % ("LSTM" if self.spec.cell == "lstm" else "GRU")}
+
+    def check(self, out):
+        """max-abs of the timed path's output against the float64 oracle."""
+        import numpy as np
+
+        from oracle.rnn_ref import rnn_forward_ref
+
+        ref = rnn_forward_ref(self.spec.cell, self.x.double().numpy(),
+                              [{k: v.double().numpy() for k, v in d.items()} for d in self.weights], dirs=self.spec.dirs)
+        return max(float(np.abs(o.double().numpy() - r).max()) for o, r in zip(out, ref) if r is not None)
+
+    def describe(self):
+        s, f = self.spec, self.full
+        part = f"{s.batch} of {f.batch} sequences" + (f", first {s.seq} of {f.seq} timesteps (value scaled to T={f.seq})"
+                                                       if s.seq < f.seq else f", full T={f.seq}")
+        return (f"{spec_name(f)} cell DAG ({s.layers * s.dirs * s.seq} cells) in Plan.order of the latency-optimal plan "
+                f"({self.planner_src} planner, cpu-comparable profile), one torch fp32 dispatch per cell, "
+                f"{self.threads} threads; {part}")
+
+
+def time_cpu_baseline(spec, budget_s: float, sample_batch: int, sample_seq: int = 0):
+    """The host reference (HostReference) on the host cores, bounded to ~budget_s seconds."""
+    hr = HostReference(spec, sample_batch, sample_seq)
     t0 = time.perf_counter()
-    oracle_forward_sample(spec, w, x)  # warm (BLAS thread pool)
+    out = hr.step()  # warm (thread pool)
     first = time.perf_counter() - t0
     reps = max(1, min(20, int(budget_s / max(first, 1e-3))))
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        oracle_forward_sample(spec, w, x)
+        hr.step()
         times.append(time.perf_counter() - t0)
     p50 = statistics.median(times)
-    return {"value": sample_batch / p50, "unit": UNIT, "p50_ms": p50 * 1e3, "reps": reps,
-            "sample": f"{spec_name(spec)} forward on {sample_batch} of {spec.batch} sequences (full T={spec.seq}, L={spec.layers}), float64 numpy oracle, median of {reps}"}
-
-
-def torch_cpu_reference(spec, sample_batch, reps=3):
-    """Fused torch.nn.LSTM fp32 on the host (best-case CPU path, context only)."""
-    import torch
-
-    from paper_2307_11339_b200 import init_weights, make_input
-
-    cls = torch.nn.LSTM if spec.cell == "lstm" else torch.nn.GRU
-    m = cls(spec.I, spec.hidden, spec.layers, bidirectional=spec.dirs == 2)
-    x = make_input(spec, 1)[:, :sample_batch].contiguous()
-    with torch.no_grad():
-        m(x)
-        ts = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            m(x)
-            ts.append(time.perf_counter() - t0)
-    p50 = statistics.median(ts)
-    return {"value": sample_batch / p50, "p50_ms": p50 * 1e3, "threads": torch.get_num_threads()}
+    return {"value": hr.spec.batch * hr.seq_scale / p50, "unit": UNIT, "p50_ms": p50 * 1e3, "reps": reps,
+            "cores": hr.threads, "sample": hr.describe() + f", median of {reps}",
+            "max_abs_vs_f64_oracle": hr.check(out), "torch_fused_fp32": hr.time_fused()}
 
 
 def time_planner(mod, spec, reps=3):
@@ -315,33 +350,33 @@ def run_pipeline(args, spec, world, rank, local, dev):
 
 
 def run_reference(args, spec):
+    """The reference arm: BASELINE.md §2's host-CPU path (fp32 torch,
+    cell-by-cell in Plan.order, all host threads) on rank 0; other ranks exit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np  # noqa: F401
-
     info = cpu_info()
-    sample_batch = args.ref_sample_batch
-    w, x = cpu_sample_setup(spec, sample_batch)
+    hr = HostReference(spec, args.ref_sample_batch, args.ref_sample_seq)
     for _ in range(args.warmup):
-        oracle_forward_sample(spec, w, x)
+        out = hr.step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle_forward_sample(spec, w, x)
+        out = hr.step()
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = sample_batch * args.steps / total
+    value = hr.spec.batch * hr.seq_scale * args.steps / total
     p50 = statistics.median(times) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "p50_ms": p50,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {describe(spec)} forward; reference-arm step = {sample_batch}-sequence sample",
-                   "batch_per_gpu": spec.batch, "sample_batch": sample_batch},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["affinity"], "kind": "port",
-                         "sample": f"float64 numpy oracle (oracle/rnn_ref.py) cell DAG forward on {sample_batch} sequences, all host threads via BLAS",
-                         "host": info},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {describe(spec)} forward; reference-arm step = the host sample below",
+                   "batch_per_gpu": spec.batch, "sample_batch": hr.spec.batch, "sample_seq": hr.spec.seq},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": hr.threads, "kind": "port",
+                         "sample": hr.describe(), "host": info,
+                         "max_abs_vs_f64_oracle": hr.check(out), "tolerance": 1e-4,
+                         "torch_fused_fp32": hr.time_fused()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     hs = reference_planner()
@@ -362,6 +397,7 @@ def main(argv=None):
     ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
     ap.add_argument("--cpu-sample-batch", type=int, default=64)
     ap.add_argument("--ref-sample-batch", type=int, default=64)
+    ap.add_argument("--ref-sample-seq", type=int, default=0, help="host sample: timestep prefix (0 = full T)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["shard", "pipeline"], default="shard",
                     help="shard: N independent request shards (weak scaling); pipeline: layers split over N GPUs")
@@ -499,14 +535,11 @@ def main(argv=None):
 
         line["planner"] = dict(time_planner(pkg, spec), note="this package's planner (bit-exact with the reference)")
     if world == 1 and not args.no_cpu_baseline:
-        info = cpu_info()
-        cb = time_cpu_baseline(spec, args.cpu_baseline_seconds, args.cpu_sample_batch)
-        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": info["affinity"], "kind": "port",
-                                "sample": cb["sample"], "p50_ms": cb["p50_ms"], "host": info}
-        try:
-            line["cpu_baseline"]["torch_fused_fp32"] = torch_cpu_reference(spec, args.cpu_sample_batch)
-        except Exception as exc:  # context only
-            line["cpu_baseline"]["torch_fused_fp32"] = {"error": str(exc)}
+        cb = time_cpu_baseline(spec, args.cpu_baseline_seconds, args.cpu_sample_batch, args.ref_sample_seq)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                                "sample": cb["sample"], "p50_ms": cb["p50_ms"], "host": cpu_info(),
+                                "max_abs_vs_f64_oracle": cb["max_abs_vs_f64_oracle"],
+                                "torch_fused_fp32": cb["torch_fused_fp32"]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

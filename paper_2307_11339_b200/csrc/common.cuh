@@ -10,6 +10,69 @@ namespace hs {
 // (hs_rnn_last_launch_count; reset at the start of every forward entry point)
 inline thread_local int g_launch_count = 0;
 
+// Per-device one-time setup (cudaFuncSetAttribute and lazy module loading act
+// on the current device only): flags are indexed by the current device.
+constexpr int kMaxDev = 16;
+inline int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) d = 0;
+  return d;
+}
+
+// ------------------------------------------------------------------ watchdog
+// Every spin on a value another CTA or another kernel publishes (per-chunk h
+// counters, XP readiness, the dynamic K1's progress poll, the SIMT grid
+// barrier) is bounded: if the awaited condition has not held for
+// g_watchdog_ns (HS_WATCHDOG_MS, default 10 s; 0 = off) the spinning thread
+// records where it was in a host-mapped word and traps.  A lost co-residency
+// (another process / MPS client holding the SMs a persistent launch counted
+// on) then surfaces as a CUDA error with a message (hs_last_error) instead of
+// a silent hang.  Sites:
+enum WatchSite : unsigned int {
+  kWatchRecurChunk = 1,   // recurrence producer: h_{t-1} chunk counter
+  kWatchRecurXready = 2,  // recurrence: K1 tiles of the next timestep (XP streaming)
+  kWatchGemmProgress = 3, // dynamic K1: recurrence progress for the tile's rows
+  kWatchGridBarrier = 4,  // SIMT recurrence grid barrier
+  kWatchPeerFlag = 5,     // pipeline hand-off: previous stage's step flag
+};
+__device__ unsigned long long g_watchdog_ns = 0;
+__device__ unsigned int* g_watch_word = nullptr;  // host-mapped; 0 = no event
+
+__device__ __noinline__ void watchdog_fire(unsigned int site) {
+  unsigned int* w = g_watch_word;
+  if (w) {
+    atomicCAS_system(w, 0u, 0x80000000u | ((blockIdx.x & 0xffffu) << 8) | (site & 0xffu));
+    __threadfence_system();
+  }
+  __trap();
+}
+
+struct Spin {
+  unsigned long long t0 = 0;
+  unsigned int n = 0;
+  // call once per unsuccessful poll
+  __device__ __forceinline__ void tick(unsigned int site) {
+    if ((++n & 63u) != 0u) return;
+    const unsigned long long lim = g_watchdog_ns;
+    if (lim == 0ull) return;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 == 0ull) t0 = now;
+    else if (now - t0 > lim) watchdog_fire(site);
+  }
+};
+
+// spin until *p >= target (acquire, gpu scope), bounded by the watchdog
+__device__ __forceinline__ unsigned int wait_geq(const unsigned int* p, unsigned int target, unsigned int site) {
+  unsigned int v;
+  Spin sp;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) return v;
+    sp.tick(site);
+  }
+}
+
 // Full-precision activations: the f32 mode is held to max-abs 1e-4 against
 // the float64 oracle, so no __expf / tanh.approx here.
 __device__ __forceinline__ float sigmoidf_(float v) { return 1.0f / (1.0f + expf(-v)); }
@@ -31,10 +94,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int tar
   if (threadIdx.x == 0) {
     __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
-    unsigned int seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
-    } while (seen < target);
+    wait_geq(ctr, target, kWatchGridBarrier);
     __threadfence();
   }
   __syncthreads();

@@ -24,6 +24,50 @@ namespace {
 
 thread_local std::string g_err;
 
+// ---- watchdog (common.cuh): one host-mapped event word per device
+std::mutex g_watch_mu;
+unsigned int* g_watch_host[hs::kMaxDev] = {};
+
+// Set up the device-side watchdog once per device: the host-mapped event word
+// and the timeout (HS_WATCHDOG_MS, default 10000; 0 disables).
+cudaError_t watchdog_init(int dev) {
+  std::lock_guard<std::mutex> lk(g_watch_mu);
+  if (g_watch_host[dev]) return cudaSuccess;
+  unsigned int* h = nullptr;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(unsigned int), cudaHostAllocMapped);
+  if (e != cudaSuccess) return e;
+  *h = 0u;
+  void* d = nullptr;
+  if ((e = cudaHostGetDevicePointer(&d, h, 0)) != cudaSuccess) return e;
+  const char* env = getenv("HS_WATCHDOG_MS");
+  const unsigned long long ns = (env ? strtoull(env, nullptr, 10) : 10000ull) * 1000000ull;
+  if ((e = cudaMemcpyToSymbol(hs::g_watch_word, &d, sizeof(d))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(hs::g_watchdog_ns, &ns, sizeof(ns))) != cudaSuccess) return e;
+  g_watch_host[dev] = h;
+  return cudaSuccess;
+}
+
+// Describe a watchdog event recorded on any device ("" if none).
+std::string watchdog_note() {
+  static const char* sites[] = {"?", "recurrence h-chunk counter", "recurrence XP readiness (K1 tiles)",
+                                "dynamic K1 progress poll", "SIMT grid barrier", "pipeline peer flag"};
+  for (int d = 0; d < hs::kMaxDev; ++d) {
+    const unsigned int* h = g_watch_host[d];
+    if (!h) continue;
+    const unsigned int w = *reinterpret_cast<const volatile unsigned int*>(h);
+    if (!w) continue;
+    const unsigned int site = w & 0xffu;
+    char buf[320];
+    snprintf(buf, sizeof buf,
+             " [watchdog on device %d: a spin at '%s' (block %u) saw no progress for HS_WATCHDOG_MS; "
+             "the persistent kernels lost co-residency (another client holding SMs?) or a peer faulted. "
+             "The CUDA context is unusable; restart the process]",
+             d, sites[site < 6 ? site : 0], (w >> 8) & 0xffffu);
+    return buf;
+  }
+  return "";
+}
+
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -32,6 +76,7 @@ int fail(int code, const char* fmt, ...) {
   vsnprintf(buf, sizeof(buf), fmt, ap);
   va_end(ap);
   g_err = buf;
+  if (code == HS_ERR_CUDA) g_err += watchdog_note();
   return code;
 }
 
@@ -90,6 +135,7 @@ int device_info(DeviceInfo* info) {
     HS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     n.smem_optin = optin;
     if (n.cc_major != 10) return fail(HS_ERR_NO_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a only", dev, n.cc_major, n.cc_minor);
+    HS_CUDA(watchdog_init(dev));
     HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.occ_simt4, hs::recur_simt<4>, hs::RTHREADS, sizeof(hs::RecurSmem<4>)));
     HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.occ_simt3, hs::recur_simt<3>, hs::RTHREADS, sizeof(hs::RecurSmem<3>)));
     c = n;
@@ -224,7 +270,8 @@ int launch_small(const Dims& m, const hs::SmallArgs& sa, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (m.G == 4) {
-    static bool init = false;
+    static bool init_d[hs::kMaxDev] = {};
+    bool& init = init_d[hs::cur_device()];
     if (!init) {
       HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
       HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -232,7 +279,8 @@ int launch_small(const Dims& m, const hs::SmallArgs& sa, cudaStream_t s) {
     }
     HS_CUDA(cudaLaunchKernelEx(&cfg, hs::recur_cluster_small<4>, sa));
   } else {
-    static bool init = false;
+    static bool init_d[hs::kMaxDev] = {};
+    bool& init = init_d[hs::cur_device()];
     if (!init) {
       HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
       HS_CUDA(cudaFuncSetAttribute(hs::recur_cluster_small<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -282,16 +330,26 @@ struct Overlap {
 // waits only for that — not for the whole previous forward — so a caller
 // alternating two staging buffers overlaps request k+1's upload with
 // request k's compute.
+// Keyed by (device, buffer): events belong to a device.  The cache is per host
+// thread, like the internal streams, so one executor's request stream must be
+// driven from one thread ("Streams and concurrency").
 int x_free_event(const void* x_dev, cudaEvent_t* ev, bool* seen) {
-  struct Entry { const void* p; cudaEvent_t ev; };
+  struct Entry { const void* p; int dev; cudaEvent_t ev; };
   static thread_local Entry cache[8] = {};
   static thread_local int next = 0;
+  int dev = 0;
+  HS_CUDA(cudaGetDevice(&dev));
   for (auto& e : cache)
-    if (e.p == x_dev && e.ev) { *ev = e.ev; *seen = true; return HS_OK; }
+    if (e.p == x_dev && e.dev == dev && e.ev) { *ev = e.ev; *seen = true; return HS_OK; }
   Entry& e = cache[next];
   next = (next + 1) % 8;
+  if (e.ev && e.dev != dev) {  // slot held an event of another device
+    cudaEventDestroy(e.ev);
+    e.ev = nullptr;
+  }
   if (!e.ev) HS_CUDA(cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming));
   e.p = x_dev;
+  e.dev = dev;
   *ev = e.ev;
   *seen = false;
   return HS_OK;
@@ -690,6 +748,13 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     a.ypl = last ? nullptr : xpl;
     a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
+    // HS_TEST_STALL=1 (watchdog test only): layer 0 waits for K1 tiles that
+    // never come, so its first XP poll can only end through the watchdog
+    static const bool test_stall = getenv("HS_TEST_STALL") != nullptr;
+    if (test_stall && l == 0) {
+      a.xready = xready;
+      a.xready_target = 0xffffffffu;
+    }
     static const char* trace_path = getenv("HS_RECUR_TRACE");
     a.trace = trace_path && l == 0 ? reinterpret_cast<unsigned long long*>(tcws + tw.trace) : nullptr;
     if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
@@ -944,6 +1009,11 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     }
     if (nev) HS_CUDA(cudaEventRecord(evs[2 * l + 2], s));
   }
+  // everything enqueued on the K1 stream (the last layer's side K1 in XP
+  // streaming) is joined back to the caller's stream: stream order on `s`
+  // covers the whole forward, and the next forward's counter zeroing on `s`
+  // cannot overtake a side K1 still claiming tiles
+  if (gs && (rc = join(gs, s))) return rc;
   if (xstream && (rc = xp_update(xp_key, m.T))) return rc;  // the GPU has the last layer to run meanwhile
   if (nev) {
     HS_CUDA(cudaEventSynchronize(evs[nev - 1]));

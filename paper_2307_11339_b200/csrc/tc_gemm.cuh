@@ -13,6 +13,7 @@
 //   warp 2   TMEM allocator (BN f32 columns)
 //   warps 4-7 epilogue: tcgen05.ld 32x32b -> +bias -> st.global f32
 #pragma once
+#include "common.cuh"
 #include "tc_common.cuh"
 
 namespace hs {
@@ -353,10 +354,7 @@ __global__ void __launch_bounds__(256, 1)
         const int t0 = m0 / g.B, t1 = min(g.T, (m0 + GBM + g.B - 1) / g.B);
         const int s_need = g.D == 1 ? t1 - 1 : max(t1 - 1, g.T - 1 - t0);
         if (g.progress) {  // nullptr: every row is already in memory
-          unsigned int seen;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.progress + s_need) : "memory");
-          } while (seen < g.ncta);
+          wait_geq(g.progress + s_need, g.ncta, kWatchGemmProgress);
           ptx::fence_proxy_async_global();  // generic-proxy y stores -> TMA reads
         }
         const CUtensorMap* tb = d == 0 ? &tmB0 : &tmB1;

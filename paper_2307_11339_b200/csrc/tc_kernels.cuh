@@ -296,23 +296,25 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   cudaError_t e;
   static const char* np_env = getenv("HS_GEMM_NONPERSISTENT");  // A/B runs
   if (BN == 256 && persistent && !np_env) {
-    static bool initp = false;
-    static int sms = 0;
-    if (!initp) {
+    static bool initp_d[kMaxDev] = {};
+    static int sms_d[kMaxDev] = {};
+    const int dev = cur_device();
+    if (!initp_d[dev]) {
       if ((rc = set_smem(gemm_xproj_persistent, gemm_p_smem_bytes(), err))) return rc;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      initp = true;
+      cudaDeviceGetAttribute(&sms_d[dev], cudaDevAttrMultiProcessorCount, dev);
+      initp_d[dev] = true;
     }
+    const int sms = sms_d[dev];
     const int tiles = (int)(grid.x * grid.y);
     gemm_xproj_persistent<<<tiles < sms ? tiles : sms, 256, gemm_p_smem_bytes(), s>>>(ta, tb, bias, C, M, N, K, npass);
   } else if (BN == 256) {
-    static bool init = false;
+    static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
     if (!init) { if ((rc = set_smem(gemm_xproj_kernel<256>, gemm_smem_bytes<256>(), err))) return rc; init = true; }
     gemm_xproj_kernel<256><<<grid, 256, gemm_smem_bytes<256>(), s>>>(ta, tb, bias, C, M, N, K, npass);
   } else {
-    static bool init = false;
+    static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
     if (!init) { if ((rc = set_smem(gemm_xproj_kernel<128>, gemm_smem_bytes<128>(), err))) return rc; init = true; }
     gemm_xproj_kernel<128><<<grid, 256, gemm_smem_bytes<128>(), s>>>(ta, tb, bias, C, M, N, K, npass);
   }
@@ -328,7 +330,8 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
 // Overlapped K1 of the next layer (gemm_xproj_dyn): one CTA per SM on stream
 // s, launched once the recurrence is resident; *claim must be zeroed before.
 inline int gemm_dyn_preload(std::string& err) {  // loads the module (lazy loading) + smem opt-in, once
-  static bool init = false;
+  static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
   if (!init) {
     int rc = set_smem(gemm_xproj_dyn, gemm_d_smem_bytes(), err);
     if (rc) return rc;
@@ -400,7 +403,8 @@ inline cudaError_t occ_clusters(int* n, K kernel, const cudaLaunchConfig_t& cfg)
 
 template <int G, int NPL>
 inline int max_coresident_ctas_t(int S, size_t smem) {
-  static bool init = false;
+  static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
   std::string err;
   if (!init) {
     if (set_smem(recur_tc_kernel<G, NPL, 1, 0>, kSmemMax, err)) return 0;
@@ -431,10 +435,17 @@ inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
   return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
 }
 
+// persistent recurrences launch cooperatively (HS_COOP=0: plain cluster launch, A/B only)
+inline bool coop_launch() {
+  static const char* env = getenv("HS_COOP");
+  return !(env && atoi(env) == 0);
+}
+
 template <int G, int NPL, int CELLS, int NSW>
 inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
                         int S, size_t smem, cudaStream_t s, std::string& err) {
-  static bool init = false;
+  static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
   int rc;
   if (!init) {
     if ((rc = set_smem(recur_tc_kernel<G, NPL, CELLS, NSW>, kSmemMax, err))) return rc;
@@ -445,7 +456,7 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
   cfg.blockDim = dim3(kRecurThreads + (NSW ? 32 : 0));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = S;
   attr[0].val.clusterDim.y = 1;
@@ -463,6 +474,11 @@ inline int launch_recur(const CUtensorMap& w0, const CUtensorMap& w1, const CUte
           std::to_string(S) + ", device fits " + std::to_string(nclusters);
     return 3;
   }
+  // cooperative: every CTA of the persistent grid is resident at once or the
+  // launch waits / fails — never a partial grid spinning on absent peers
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.numAttrs = coop_launch() ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, recur_tc_kernel<G, NPL, CELLS, NSW>, w0, w1, hm, a);
   if (e != cudaSuccess) {
     err = std::string("recur_tc_kernel launch: ") + cudaGetErrorString(e);
@@ -565,7 +581,8 @@ inline int choose_split2(int G, int H, int B, int D, int NPL) {
 template <int G, int NPL, int CELLS>
 inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUtensorMap& hm, const TcRecurArgs& a,
                          int S, size_t smem, cudaStream_t s, std::string& err) {
-  static bool init = false;
+  static bool init_d[kMaxDev] = {};
+  bool& init = init_d[cur_device()];
   int rc;
   if (!init) {
     if ((rc = set_smem(recur_tc2_kernel<G, NPL, CELLS>, kSmemMax, err))) return rc;
@@ -576,7 +593,7 @@ inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUt
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = S;
   attr[0].val.clusterDim.y = 1;
@@ -589,6 +606,9 @@ inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUt
     err = "two-group recurrent kernel cannot be co-resident";
     return 3;
   }
+  attr[1].id = cudaLaunchAttributeCooperative;  // whole grid resident (see launch_recur)
+  attr[1].val.cooperative = 1;
+  cfg.numAttrs = coop_launch() ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, recur_tc2_kernel<G, NPL, CELLS>, w0, w1, hm, a);
   if (e != cudaSuccess) {
     err = std::string("recur_tc2_kernel launch: ") + cudaGetErrorString(e);

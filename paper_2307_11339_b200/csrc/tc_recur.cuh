@@ -63,12 +63,7 @@ struct TcRecurArgs {
 __device__ __forceinline__ void wait_xready(const TcRecurArgs& a, int tt) {
   if (!a.xready) return;
   const int lo = (tt * a.Bst) / 128, hi = (tt * a.Bst + a.Bst - 1) / 128;
-  for (int mt = lo; mt <= hi; ++mt) {
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.xready + mt) : "memory");
-    } while (v < a.xready_target);
-  }
+  for (int mt = lo; mt <= hi; ++mt) wait_geq(a.xready + mt, a.xready_target, kWatchRecurXready);
 }
 __device__ __forceinline__ void signal_started(const TcRecurArgs& a) {
   if (a.started && threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.started) : "memory");
@@ -315,10 +310,7 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
         HS_TRACE(0);
         const unsigned int target = per_round * (unsigned int)(s + 1);
         for (int c = 0; c < nch; ++c) {
-          unsigned int seen;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter + c * kCtrStride) : "memory");
-          } while (seen < target);
+          wait_geq(in_counter + c * kCtrStride, target, kWatchRecurChunk);
           if (c == 0) HS_TRACE(1);
           if (c == nch - 1) HS_TRACE(12);
           ptx::fence_proxy_async_global();

@@ -207,10 +207,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         const unsigned int target = per_round * (unsigned int)(s + 1);
         for (int c = 0; c < nch; ++c) {
-          unsigned int seen;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(in_counter + c * kCtrStride) : "memory");
-          } while (seen < target);
+          wait_geq(in_counter + c * kCtrStride, target, kWatchRecurChunk);
           if (grp == 0 && c == 0) HS_TRACE(1);
           if (grp == 0 && c == nch - 1) HS_TRACE(12);
           ptx::fence_proxy_async_global();

@@ -253,8 +253,8 @@ def _execute_fused(graph, sched, ex, x, h0, c0) -> ExecResult:
     spec = ex.spec
     dev = ex.device
     x = x.to(dev, torch.float32).contiguous()
-    h0 = h0.to(dev).contiguous() if h0 is not None else None
-    c0 = c0.to(dev).contiguous() if c0 is not None else None
+    h0 = h0.to(dev, torch.float32).contiguous() if h0 is not None else None
+    c0 = c0.to(dev, torch.float32).contiguous() if c0 is not None else None
     y, hn, cn, lm = ex.forward(x, h0, c0, layer_ms=True)
     T, D = spec.seq, spec.dirs
     spans = []

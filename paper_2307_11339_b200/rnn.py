@@ -292,6 +292,19 @@ class RNNExecutor:
         cn = torch.empty_like(hn) if s.cell == "lstm" else None
         return y, hn, cn
 
+    def _check_dev(self, name, t, shape, required=False):
+        """Every tensor handed to the library as a raw pointer: float32,
+        contiguous, on this executor's device, of the expected shape."""
+        if t is None:
+            if required:
+                raise ValueError(f"{name} is required")
+            return
+        if t.device != self.device or t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous float32 tensor on {self.device} "
+                             f"(got {t.dtype} on {t.device}, contiguous={t.is_contiguous()})")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
     def forward(self, x: torch.Tensor, h0=None, c0=None, out=None, layer_ms: bool = False):
         """Run the DAG on device tensors.  Returns ``(y, h_n, c_n)`` (c_n None
         for GRU), plus per-layer [gemm_ms, recurrent_ms] when ``layer_ms``."""
@@ -300,7 +313,13 @@ class RNNExecutor:
             raise ValueError("x must be a contiguous float32 tensor on the executor's device")
         if tuple(x.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"x has shape {tuple(x.shape)}, expected {(s.seq, s.batch, s.I)}")
+        state = (s.layers * s.dirs, s.batch, s.hidden)
+        self._check_dev("h0", h0, state)
+        self._check_dev("c0", c0 if s.cell == "lstm" else None, state)
         y, hn, cn = out if out is not None else self.alloc_outputs()
+        self._check_dev("y", y, (s.seq, s.batch, s.dirs * s.hidden), required=True)
+        self._check_dev("h_n", hn, state, required=True)
+        self._check_dev("c_n", cn, state, required=s.cell == "lstm")
         times = (ctypes.c_float * (2 * s.layers))() if layer_ms else None
         ptr = lambda t: t.data_ptr() if t is not None else None
         with torch.cuda.device(self.device):
@@ -337,18 +356,29 @@ class RNNExecutor:
         if tuple(x_host.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"x has shape {tuple(x_host.shape)}, expected {(s.seq, s.batch, s.I)}")
         y, hn, cn = out_host if out_host is not None else self.alloc_host_outputs()
+        state = (s.layers * s.dirs, s.batch, s.hidden)
+        for name, t, shp, req in (("y", y, (s.seq, s.batch, s.dirs * s.hidden), True), ("h_n", hn, state, True),
+                                  ("c_n", cn, state, s.cell == "lstm"), ("h0", h0, state, False),
+                                  ("c0", c0, state, False)):
+            if t is None:
+                if req:
+                    raise ValueError(f"{name} is required")
+                continue
+            if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or tuple(t.shape) != shp:
+                raise ValueError(f"{name} must be a contiguous float32 host tensor of shape {shp}")
         if staging is None:
             staging = self.alloc_staging()
         xd, (yd, hnd, cnd), state = staging
         ptr = lambda t: t.data_ptr() if t is not None else None
-        self.desc.upload_chunks = int(upload_chunks)
+        desc = make_desc(s)  # per call: concurrent callers never share a mutated descriptor
+        desc.upload_chunks = int(upload_chunks)
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device)
             _check(
                 self.lib,
                 "hs_rnn_forward_host",
                 self.lib.hs_rnn_forward_host(
-                    ctypes.byref(self.desc), self.packed.data_ptr(), x_host.data_ptr(), ptr(h0), ptr(c0),
+                    ctypes.byref(desc), self.packed.data_ptr(), x_host.data_ptr(), ptr(h0), ptr(c0),
                     y.data_ptr(), hn.data_ptr(), ptr(cn), xd.data_ptr(), yd.data_ptr(), hnd.data_ptr(), ptr(cnd),
                     state.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), stream.cuda_stream,
                 ),

@@ -70,15 +70,15 @@ class RNNServer:
         staging = self.staging[slot]
         host_outs = self.host_outs[slot]
         if req.x.device.type == "cpu":
-            h0 = req.h0.contiguous() if req.h0 is not None else None
-            c0 = req.c0.contiguous() if req.c0 is not None else None
-            ex.forward_host(req.x.contiguous(), h0, c0, out_host=host_outs, staging=staging, upload_chunks=upload_chunks)
+            h0 = req.h0.to(torch.float32).contiguous() if req.h0 is not None else None
+            c0 = req.c0.to(torch.float32).contiguous() if req.c0 is not None else None
+            ex.forward_host(req.x.to(torch.float32).contiguous(), h0, c0, out_host=host_outs, staging=staging, upload_chunks=upload_chunks)
             h2d = sum(t.numel() * t.element_size() for t in (req.x, h0, c0) if t is not None)
         else:
             dev = ex.device
             outs = staging[1]
-            ex.forward(req.x, None if req.h0 is None else req.h0.to(dev), None if req.c0 is None else req.c0.to(dev),
-                       out=outs)
+            dev_t = lambda t: None if t is None else t.to(dev, torch.float32).contiguous()
+            ex.forward(dev_t(req.x), dev_t(req.h0), dev_t(req.c0), out=outs)
             for dst, src in zip(host_outs, outs):
                 if src is not None:
                     dst.copy_(src, non_blocking=True)
