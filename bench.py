@@ -60,6 +60,8 @@ class ClockSampler:
 
     def __enter__(self):
         exe = shutil.which("nvidia-smi")
+        if not exe:
+            self._start_nvml()
         if exe:
             self.proc = subprocess.Popen(
                 [exe, f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
@@ -75,7 +77,46 @@ class ClockSampler:
             if len(parts) == 6:
                 self.samples.append(parts)
 
+    def _start_nvml(self):
+        """No nvidia-smi binary on PATH: the same fields through NVML (nvidia_ml_py)."""
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return
+        bits = [getattr(nv, n, 0) for n in ("nvmlClocksEventReasonHwSlowdown", "nvmlClocksEventReasonHwThermalSlowdown",
+                                            "nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksEventReasonSwPowerCap")]
+        self._stop = threading.Event()
+
+        def sample():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            except Exception:
+                return
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                r = 0
+            self.samples.append([str(sm), str(mx)] + ["Active" if (b and r & b) else "Not Active" for b in bits])
+
+        def poll():
+            while not self._stop.wait(0.01):
+                sample()
+
+        sample()  # at entry, after the warm-up: the clocks the timed region starts at
+
+        self._sample = sample  # also taken on exit: short timed regions still get a reading under load
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+
     def __exit__(self, *exc):
+        if getattr(self, "_stop", None) is not None:
+            self._sample()
+            self._stop.set()
         if self.proc:
             self.proc.terminate()
             try:

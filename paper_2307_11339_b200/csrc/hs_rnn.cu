@@ -19,6 +19,7 @@
 #include "cluster_small.cuh"
 #include "simt_kernels.cuh"
 #include "tc_kernels.cuh"
+#include "tc_wave.cuh"
 
 namespace {
 
@@ -213,8 +214,57 @@ int pack_layout(const Dims& m, PackLayout* p) {
 
 // ----------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t xproj, xproj2, act0, act1, cst, zeros, barrier, tc, total;
+  size_t xproj, xproj2, act0, act1, cst, zeros, barrier, tc, wave, total;
 };
+
+// ---- single-GPU layer wavefront (tc_wave.cuh): feasibility and workspace
+// Recurrence K-split of the wave for this shape (static device limits), 0 = the
+// layers run one launch after another.  Unidirectional, unsliced, every layer's
+// W_hh slices resident on chip at once, the K1 on 256-wide tiles.
+int wave_split(const Dims& m) {
+  static const char* env = getenv("HS_WAVE");  // HS_WAVE=0: layer-by-layer schedule (A/B)
+  if (env && atoi(env) == 0) return 0;
+  const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
+  if (m.D != 1 || m.L < 2 || m.L > hs::tc::kMaxWave) return 0;
+  if (!hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H, m.D, NPL)) return 0;
+  if (hs::tc::gemm_bn(m.G * m.H) != 256) return 0;
+  if (hs::tc::batch_slice(m.G, m.H, m.B, m.D, NPL) != m.B) return 0;
+  return hs::tc::choose_wave_split(m.G, m.H, m.B, m.L, NPL, m.G * m.H, hs::tc::static_cta_limit);
+}
+
+// Per-layer buffers of the wave (offsets into the workspace).  Layer 0 and 1
+// keep their XP in WsLayout::xproj / xproj2; `ctl` .. ctl + ctl_bytes is the
+// block zeroed before every wave (exchange planes, counters, claim).
+struct WaveWs {
+  size_t xproj[hs::tc::kMaxWave], ypl[hs::tc::kMaxWave];
+  size_t hbuf[hs::tc::kMaxWave], counters[hs::tc::kMaxWave], progress[hs::tc::kMaxWave], xready[hs::tc::kMaxWave];
+  size_t claim, ctl, ctl_bytes, bytes;
+};
+WaveWs wave_ws(const Dims& m, size_t base, size_t xproj0, size_t xproj1) {
+  WaveWs w{};
+  if (!wave_split(m)) return w;
+  const size_t TB = (size_t)m.T * m.B;
+  size_t off = base;
+  for (int l = 0; l < m.L; ++l) {
+    w.xproj[l] = l == 0 ? xproj0 : l == 1 ? xproj1 : off;
+    if (l >= 2) off = align_up(off + sizeof(float) * TB * m.G * m.H);
+    if (l < m.L - 1) {
+      w.ypl[l] = off;
+      off = align_up(off + 2 * TB * m.H * 2);  // bf16 hi/lo planes of layer l's output
+    }
+  }
+  w.ctl = off;
+  for (int l = 0; l < m.L; ++l) {
+    w.hbuf[l] = off;     off = align_up(off + 3 * (size_t)hs::tc::pad16(m.B) * m.H * 2);
+    w.counters[l] = off; off = align_up(off + 128 * 128);
+    w.progress[l] = off; off = align_up(off + (size_t)m.T * 4);
+    w.xready[l] = off;   off = align_up(off + ((TB + 127) / 128) * 4);
+  }
+  w.claim = off;         off = align_up(off + 4);
+  w.ctl_bytes = off - w.ctl;
+  w.bytes = off - base;
+  return w;
+}
 
 WsLayout ws_layout(const Dims& m) {
   WsLayout w{};
@@ -230,6 +280,7 @@ WsLayout ws_layout(const Dims& m) {
   w.zeros = off;   off = align_up(off + sizeof(float) * m.D * m.B * m.H);
   w.barrier = off; off = align_up(off + 256);
   w.tc = off;      off = align_up(off + hs::tc::workspace_bytes(m.G, m.H, m.B, m.T, m.D, m.in_size(0)));
+  w.wave = off;    off += wave_ws(m, off, w.xproj, w.xproj2).bytes;
   w.total = off;
   return w;
 }
@@ -568,6 +619,161 @@ inline void chunk_bounds(int T, int n, int k, int* t0, int* t1) {
   *t1 = (int)((long)T * (k + 1) / n);
 }
 
+// The layers of a unidirectional forward as ONE layer-wavefront launch
+// (tc_wave.cuh): every layer's recurrence plus the input projections, layer 0's
+// included unless the host-upload prologue already computed it (chunked_in).
+// x is already split into bf16 planes (xpl).  With host buffers (ov->y_host) y
+// drains in time chunks behind the last layer's progress counters.
+int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const void* packed, const float* x,
+                const float* h0, const float* c0, float* y, float* hn, float* cn, void* ws, const WsLayout& wl,
+                cudaStream_t s, cudaStream_t gs, const Overlap* ov, bool chunked_in, bool xreq_ok, int wS,
+                cudaEvent_t* evs, int nev, float* layer_ms) {
+  using namespace hs::tc;
+  (void)x;
+  int rc;
+  const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
+  const size_t TB = (size_t)m.T * m.B;
+  const WaveWs ww = wave_ws(m, wl.wave, wl.xproj, wl.xproj2);
+  const TcWs tw = tc_ws_layout(m.G, m.H, m.B, m.T, m.D, m.I);
+  __nv_bfloat16* xpl = reinterpret_cast<__nv_bfloat16*>(at<unsigned char>(ws, wl.tc) + tw.xpl);
+  float* zeros = at<float>(ws, wl.zeros);
+  // HS_WAVE_K1L0=1 (A/B): layer 0's K1 as a full-GPU GEMM before the wave
+  static const char* k1l0_env = getenv("HS_WAVE_K1L0");
+  const bool k1_before = !chunked_in && k1l0_env && atoi(k1l0_env) == 1;
+  const int seg0 = chunked_in || k1_before ? 1 : 0;
+  if (k1_before) {
+    const LayerPack& lp = pl.ld[0];
+    rc = gemm_planes(xpl, at<__nv_bfloat16>(packed, lp.tc), at<float>(packed, lp.bias_x), at<float>(ws, ww.xproj[0]),
+                     (int)TB, m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err);
+    if (rc) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+  }
+  {
+    ZeroList zl{};
+    zl.p[0] = at<uint4>(ws, ww.ctl);
+    zl.n16[0] = ww.ctl_bytes / 16;
+    zl.k = 1;
+    zero_list_kernel<<<2 * di.sms, 256, 0, s>>>(zl);
+    HS_CUDA(cudaGetLastError());
+    ++hs::g_launch_count;
+  }
+  const bool drain = ov && ov->y_host;
+  WaitValue32Fn wait = wait_value_fn();
+  // counters are zeroed before the copy / K1 streams poll them
+  if (drain && wait && (rc = join(s, ov->cs_out))) return rc;
+  const bool gate_next = drain && wait && xreq_ok && gs;
+  if (gate_next && (rc = join(s, gs))) return rc;
+  WaveArgs wa{};
+  wa.rec.L = m.L;
+  GemmDynArgs ga{};
+  ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.H; ga.npass = NPL == 2 ? 3 : 1;
+  ga.D = 1; ga.T = m.T; ga.B = m.B;
+  ga.claim = at<unsigned int>(ws, ww.claim);
+  ga.nseg = m.L - seg0;
+  // claim-order skew between consecutive layers, in M-tiles: about 12
+  // timesteps (measured c3: a layer's step 0 trails the layer below it by
+  // ~11 steps; lag 1/2/3/4/6/8 M-tiles -> 3.51/1.78/1.59/1.63/1.71/1.79 ms)
+  static const char* lag_env = getenv("HS_WAVE_LAG");
+  ga.lag = lag_env ? atoi(lag_env) : (int)((12 * (size_t)m.B + 127) / 128);
+  const unsigned int ncta = (unsigned int)((m.H / 32) * wS);  // CTAs of one layer's recurrence
+  const __nv_bfloat16* whh[kMaxWave];
+  const __nv_bfloat16* apl[kMaxSeg];
+  const __nv_bfloat16* wih[kMaxSeg];
+  size_t apst[kMaxSeg];
+  for (int l = 0; l < m.L; ++l) {
+    const int Il = m.in_size(l);
+    const LayerPack& lp = pl.ld[l];
+    const __nv_bfloat16* wihp = at<__nv_bfloat16>(packed, lp.tc);
+    whh[l] = wihp + 2 * wih_plane_elems(m.G, m.H, Il);
+    TcRecurArgs& a = wa.rec.layer[l];
+    a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = 1; a.Bst = m.B;
+    float* xp = at<float>(ws, ww.xproj[l]);
+    a.xproj[0] = xp;
+    a.bias_h[0] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+    a.whh_scale[0] = whh_scales(at<unsigned char>(const_cast<void*>(packed), lp.tc), m.G, m.H, Il);
+    a.h0[0] = h0 ? h0 + (size_t)l * m.B * m.H : zeros;
+    a.c0[0] = c0 ? c0 + (size_t)l * m.B * m.H : zeros;
+    a.hn[0] = hn + (size_t)l * m.B * m.H;
+    a.cn[0] = cn ? cn + (size_t)l * m.B * m.H : nullptr;
+    const bool lastl = l == m.L - 1;
+    a.y = lastl ? y : nullptr;
+    a.ypl = lastl ? nullptr : at<__nv_bfloat16>(ws, ww.ypl[l]);
+    a.hbuf = at<uint16_t>(ws, ww.hbuf[l]);
+    a.counters = at<unsigned int>(ws, ww.counters[l]);
+    a.progress = at<unsigned int>(ws, ww.progress[l]);
+    if (l >= seg0) {
+      const int j = l - seg0;
+      a.xready = at<unsigned int>(ws, ww.xready[l]);
+      a.xready_target = (unsigned int)(m.G * m.H / 256);  // N-tiles per M-tile
+      apl[j] = l == 0 ? xpl : at<__nv_bfloat16>(ws, ww.ypl[l - 1]);
+      apst[j] = TB * (size_t)Il;
+      wih[j] = wihp;
+      ga.bias[j] = at<float>(packed, lp.bias_x);
+      ga.C[j] = xp;
+      ga.wK[j] = Il;
+      ga.wprogress[j] = l == 0 ? nullptr : at<unsigned int>(ws, ww.progress[l - 1]);
+      ga.wncta[j] = ncta;
+      ga.wxready[j] = at<unsigned int>(ws, ww.xready[l]);
+    }
+  }
+  // HS_RECUR_TRACE=<file>: every layer's recurrence CTAs record their first
+  // kTraceSteps steps (tools/trace_wave.py)
+  static const char* trace_path = getenv("HS_RECUR_TRACE");
+  unsigned long long* trace = nullptr;
+  if (trace_path) {
+    trace = reinterpret_cast<unsigned long long*>(at<unsigned char>(ws, wl.tc) + tw.trace);
+    HS_CUDA(cudaMemsetAsync(trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
+    for (int l = 0; l < m.L; ++l) wa.rec.layer[l].trace = trace;
+  }
+  if (nev) HS_CUDA(cudaEventRecord(evs[1], s));
+  if ((rc = launch_wave(m.G, NPL, wS, whh, wa, apl, apst, wih, ga, s, g_err)))
+    return fail(rc == 3 ? HS_ERR_UNSUPPORTED : HS_ERR_CUDA, "%s", g_err.c_str());
+  if (nev) HS_CUDA(cudaEventRecord(evs[2], s));
+  if (trace) {
+    static unsigned long long host[160 * kTraceSteps * 16];
+    HS_CUDA(cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s));
+    HS_CUDA(cudaStreamSynchronize(s));
+    FILE* f = fopen(trace_path, "wb");
+    if (f) { fwrite(host, 1, sizeof(host), f); fclose(f); }
+  }
+  if (drain) {
+    const unsigned int* plast = at<unsigned int>(ws, ww.progress[m.L - 1]);
+    if (!wait && (rc = join(s, ov->cs_out))) return rc;  // no stream memory ops: drain after the kernel
+    if (gate_next) {
+      // the next request's layer-0 K1 (request overlap, on gs) overwrites layer
+      // 0's XP: it may start once layer 0's recurrence has finished
+      CUresult r = wait(gs, reinterpret_cast<CUdeviceptr>(at<unsigned int>(ws, ww.progress[0]) + m.T - 1), ncta, 0);
+      if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    }
+    const int nco = m.T < 16 ? m.T : 16;
+    const size_t row = (size_t)m.B * m.H;
+    for (int k = 0; k < nco; ++k) {
+      int t0, t1;
+      chunk_bounds(m.T, nco, k, &t0, &t1);
+      if (wait) {
+        CUresult r = wait(ov->cs_out, reinterpret_cast<CUdeviceptr>(plast + t1 - 1), ncta, 0 /*GEQ*/);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      }
+      HS_CUDA(cudaMemcpyAsync(ov->y_host + (size_t)t0 * row, y + (size_t)t0 * row, (size_t)(t1 - t0) * row * sizeof(float),
+                              cudaMemcpyDeviceToHost, ov->cs_out));
+    }
+  }
+  if (gs && (rc = join(gs, s))) return rc;
+  if (nev) {
+    HS_CUDA(cudaEventSynchronize(evs[2]));
+    float k1 = 0.f, wv = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&k1, evs[0], evs[1]));
+    HS_CUDA(cudaEventElapsedTime(&wv, evs[1], evs[2]));
+    // one launch runs every layer: its time is shared evenly (profile_ops
+    // divides by T again, so each cell costs wave / (L*T))
+    for (int l = 0; l < m.L; ++l) {
+      layer_ms[2 * l] = l == 0 ? k1 : 0.f;
+      layer_ms[2 * l + 1] = wv / m.L;
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  }
+  return HS_OK;
+}
+
 // Tensor-core forward: per layer, split the input into bf16 planes (layer 0;
 // later layers get their planes straight from the previous recurrence
 // epilogue), K1 GEMM per direction, then one recurrent launch (both dirs).
@@ -601,6 +807,12 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   if (!Bs) return fail(HS_ERR_UNSUPPORTED, "no tensor-core recurrence plan for B=%d", m.B);
   const int nsl = (m.B + Bs - 1) / Bs;
   const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
+  // single-GPU layer wavefront (tc_wave.cuh): all layers in one cooperative launch
+  int wS = wave_split(m);
+  if (wS) {
+    const size_t wsm = wave_smem(m.G, m.H, m.B, wS, NPL);
+    if (wave_coresident(m.G, NPL, wS, wsm) / wS * wS < m.L * (m.H / 32) * wS + kWaveMinK1) wS = 0;  // co-tenant / MIG slice
+  }
   cudaStream_t gs = nullptr;
   if (overlap && (rc = gemm_stream(&gs))) return rc;
   // Request overlap (host-buffer forwards, x uploaded in one chunk): this
@@ -687,6 +899,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
   }
+  if (wS) return wave_layers(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, gs, ov, chunked_in, xreq_ok, wS, evs, nev,
+                             layer_ms);
   float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
   // XP streaming: each layer's K1 = full-GPU head over the first P timesteps,
   // then the recurrence (polling per-M-tile readiness) with the rest of K1 on
@@ -1143,6 +1357,12 @@ int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info) {
     info[1] = hs::tc::plan_split(m.G, m.H, Bs, m.D, NPL, hs::tc::static_cta_limit, &nsw);
     info[2] = nsw;
     info[3] = Bs ? (m.B + Bs - 1) / Bs : 0;
+    const int wS = wave_split(m);
+    if (wS) {  // layer wavefront: K-split of the wave's recurrences
+      info[1] = wS;
+      info[2] = 0;
+      info[5] = 1;
+    }
   } else {
     info[1] = small_cluster(m);
     info[3] = 1;

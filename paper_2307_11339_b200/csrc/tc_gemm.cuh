@@ -274,15 +274,33 @@ __global__ void __launch_bounds__(256, 1)
 // gemm_xproj_persistent (TMA ring across tiles, double-buffered TMEM
 // accumulators), plus a 16-slot tile-id queue in shared memory (tq_full
 // mbarriers) from the producer to the MMA and epilogue warps.
+constexpr int kMaxSeg = 8;  // segments of a dynamic K1 launch (directions, or the layers of a wave)
 struct GemmDynArgs {
-  const float* bias[2];            // per direction [N]
-  float* C[2];                     // per direction [M, N]
+  const float* bias[kMaxSeg];      // per segment [N]
+  float* C[kMaxSeg];               // per segment [M, N]
   int M, N, K, npass, D, T, B;
   unsigned int* claim;             // zeroed before launch
   const unsigned int* progress;    // [T] CTAs of the recurrence that finished step s
   unsigned int ncta;               // progress[s] value meaning "step s complete everywhere"
   int tile_begin, tile_end;        // claimable tile range (tile_end <= 0: all)
   unsigned int* xready;            // optional [M-tiles]: +1 per stored tile (XP streaming into a running recurrence)
+  // Wave mode (nseg > 0, D == 1): segment j is layer j+1 of a layer wavefront
+  // (recur_tc_wave_kernel).  It has its own A map (layer j's output planes),
+  // B map (layer j+1's W_ih), progress counters (layer j's steps) and xready
+  // (layer j+1's M-tiles).  Tiles are claimed along skewed diagonals: claim
+  // index u -> (k = u / per_m, segment j, N-tile n), M-tile m = k - j*lag, so
+  // a tile is claimed about when its rows are produced, and every tile a
+  // claimed tile depends on (m' <= m of segment j-1) was claimed before it.
+  int nseg, lag;
+  int wK[kMaxSeg];                 // wave mode: contraction length of each segment (layer input width)
+  const unsigned int* wprogress[kMaxSeg];
+  unsigned int wncta[kMaxSeg];
+  unsigned int* wxready[kMaxSeg];
+};
+
+struct DynMaps {
+  CUtensorMap a[kMaxSeg];  // A planes: [0] only, except in wave mode
+  CUtensorMap b[kMaxSeg];  // W_ih planes per segment
 };
 
 struct GemmDSmem {
@@ -300,22 +318,28 @@ struct GemmDSmem {
 
 constexpr size_t gemm_d_smem_bytes() { return sizeof(GemmDSmem) + 1024; }
 
-__global__ void __launch_bounds__(256, 1)
-    gemm_xproj_dyn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                   const __grid_constant__ CUtensorMap tmB1, const GemmDynArgs g) {
+// The body: also run by the K1 CTAs of the fused layer-wave kernel (tc_wave.cuh).
+__device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynArgs& g, uint8_t* smem_raw) {
   constexpr int BN = 256, ST = GemmDSmem::ST, NQ = GemmDSmem::NQ;
-  extern __shared__ uint8_t smem_raw[];
   GemmDSmem& sm = *reinterpret_cast<GemmDSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = g.K / GBK, nkb = g.npass * nk;
-  const int tiles_n = g.N / BN, per_m = g.D * tiles_n;
-  const int tiles_all = ((g.M + GBM - 1) / GBM) * per_m;
+  const bool wave = g.nseg > 0;
+  // k-blocks of a tile of segment sg (passes x K/64); the ring position is a
+  // running count because wave segments may differ in K
+  auto nkb_of = [&](int sg) -> int { return g.npass * ((wave ? g.wK[sg] : g.K) / GBK); };
+  const int nseg = wave ? g.nseg : g.D;
+  const int tiles_n = g.N / BN, per_m = nseg * tiles_n;
+  const int tiles_m = (g.M + GBM - 1) / GBM;
+  const int tiles_all = tiles_m * per_m;
   const int tiles = g.tile_end > 0 && g.tile_end < tiles_all ? g.tile_end : tiles_all;
+  const int claims = wave ? (tiles_m + (nseg - 1) * g.lag) * per_m : tiles;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&tmA);
-    ptx::tma_prefetch(&tmB0);
-    if (g.D > 1) ptx::tma_prefetch(&tmB1);
+    ptx::tma_prefetch(&mp.a[0]);
+    for (int j = 0; j < nseg; ++j) {
+      ptx::tma_prefetch(&mp.b[j]);
+      if (wave && j) ptx::tma_prefetch(&mp.a[j]);
+    }
     for (int s = 0; s < ST; ++s) {
       ptx::mbar_init(&sm.full[s], 1);
       ptx::mbar_init(&sm.empty[s], 1);
@@ -341,30 +365,46 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (ptx::elect_one()) {
+      int gi = 0;  // ring position
       for (int j = 0;; ++j) {
-        int t = g.tile_begin + (int)atomicAdd(g.claim, 1u);
-        if (t >= tiles) t = -1;
+        int t = -1;
+        for (;;) {  // next claim (wave mode skips a diagonal's out-of-range M-tiles)
+          const int u = g.tile_begin + (int)atomicAdd(g.claim, 1u);
+          if (u >= claims) break;
+          if (!wave) {
+            t = u;
+            break;
+          }
+          const int r = u % per_m, m = u / per_m - (r / tiles_n) * g.lag;
+          if (m >= 0 && m < tiles_m) {
+            t = m * per_m + r;
+            break;
+          }
+        }
         sm.tq[j % NQ] = t;
         ptx::mbar_arrive(&sm.tq_full[j % NQ]);
         if (t < 0) break;
-        const int mt = t / per_m, d = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
+        const int mt = t / per_m, sg = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
         const int m0 = mt * GBM;
         // rows [m0, m0+128) hold timesteps [t0, t1); they are final once the
         // recurrence finished step s_need (a backward direction runs T-1 .. 0)
         const int t0 = m0 / g.B, t1 = min(g.T, (m0 + GBM + g.B - 1) / g.B);
         const int s_need = g.D == 1 ? t1 - 1 : max(t1 - 1, g.T - 1 - t0);
-        if (g.progress) {  // nullptr: every row is already in memory
-          wait_geq(g.progress + s_need, g.ncta, kWatchGemmProgress);
+        const unsigned int* prog = wave ? g.wprogress[sg] : g.progress;
+        if (prog) {  // nullptr: every row is already in memory
+          wait_geq(prog + s_need, wave ? g.wncta[sg] : g.ncta, kWatchGemmProgress);
           ptx::fence_proxy_async_global();  // generic-proxy y stores -> TMA reads
         }
-        const CUtensorMap* tb = d == 0 ? &tmB0 : &tmB1;
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int gi = j * nkb + kb, st = gi % ST;
+        const CUtensorMap* ta = &mp.a[wave ? sg : 0];
+        const CUtensorMap* tb = &mp.b[sg];
+        const int nkb = nkb_of(sg), nk = nkb / g.npass;
+        for (int kb = 0; kb < nkb; ++kb, ++gi) {
+          const int st = gi % ST;
           if (gi >= ST) ptx::mbar_wait(&sm.empty[st], ((gi / ST) - 1) & 1);
           const int pass = kb / nk, kk = kb % nk;
           const int pa = pass == 2 ? 1 : 0, pb = pass == 1 ? 1 : 0;
           ptx::mbar_arrive_expect_tx(&sm.full[st], (GBM + BN) * GBK * 2);
-          ptx::tma_load_3d(sm.a[st], &tmA, &sm.full[st], kk * GBK, m0, pa);
+          ptx::tma_load_3d(sm.a[st], ta, &sm.full[st], kk * GBK, m0, pa);
           ptx::tma_load_3d(sm.b[st], tb, &sm.full[st], kk * GBK, n0, pb);
         }
       }
@@ -373,14 +413,17 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (ptx::elect_one()) {
       const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
+      int gi = 0;  // ring position
       for (int j = 0;; ++j) {
-        if (next_tile(j) < 0) break;
+        const int t = next_tile(j);
+        if (t < 0) break;
         const int buf = j & 1;
         if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int gi = j * nkb + kb, st = gi % ST;
+        const int nkb = nkb_of((t % per_m) / tiles_n);
+        for (int kb = 0; kb < nkb; ++kb, ++gi) {
+          const int st = gi % ST;
           ptx::mbar_wait(&sm.full[st], (gi / ST) & 1);
           ptx::tc_fence_after();
 #pragma unroll
@@ -400,10 +443,11 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0;; ++j) {
       const int t = next_tile(j);
       if (t < 0) break;
-      const int mt = t / per_m, d = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
+      const int mt = t / per_m, sg = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
       const int m0 = mt * GBM;
-      const float* __restrict__ bias = g.bias[d];
-      float* __restrict__ C = g.C[d];
+      const float* __restrict__ bias = g.bias[sg];
+      float* __restrict__ C = g.C[sg];
+      unsigned int* xr = wave ? g.wxready[sg] : g.xready;
       const int buf = j & 1;
       ptx::mbar_wait(&sm.tmem_full[buf], (j >> 1) & 1);
       ptx::tc_fence_after();
@@ -426,10 +470,10 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&sm.tmem_empty[buf]);
-      if (g.xready) {  // the 4 epilogue warps' stores of this tile -> one release
+      if (xr) {  // the 4 epilogue warps' stores of this tile -> one release
         ptx::named_bar(1, 128);
         if (warp == 4 && lane == 0)
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.xready + mt) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(xr + mt) : "memory");
       }
     }
   }
@@ -439,6 +483,11 @@ __global__ void __launch_bounds__(256, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
+}
+
+__global__ void __launch_bounds__(256, 1) gemm_xproj_dyn(const __grid_constant__ DynMaps mp, const GemmDynArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  gemm_dyn_body(mp, g, smem_raw);
 }
 
 // fp32 [rows, cols] (row stride ld) -> bf16 planes [2][rows][cols]; the lo

@@ -342,16 +342,38 @@ inline int gemm_dyn_preload(std::string& err) {  // loads the module (lazy loadi
 
 inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
                            const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
-  CUtensorMap ta, tb0, tb1;
-  int rc = make_map3(&ta, apl, ga.K, ga.M, 2, GBM, err, a_pstride);
-  if (!rc) rc = make_map3(&tb0, wpl[0], ga.K, ga.N, 2, 256, err);
-  if (!rc) rc = make_map3(&tb1, wpl[ga.D > 1 ? 1 : 0], ga.K, ga.N, 2, 256, err);
+  DynMaps mp;
+  int rc = make_map3(&mp.a[0], apl, ga.K, ga.M, 2, GBM, err, a_pstride);
+  for (int d = 0; d < ga.D && !rc; ++d) rc = make_map3(&mp.b[d], wpl[d], ga.K, ga.N, 2, 256, err);
   if (rc) return rc;
   if ((rc = gemm_dyn_preload(err))) return rc;
-  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(ta, tb0, tb1, ga);
+  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, ga);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("gemm_xproj_dyn launch: ") + cudaGetErrorString(e);
+    return 2;
+  }
+  ++g_launch_count;
+  return 0;
+}
+
+// Wave-mode K1 (GemmDynArgs::nseg > 0): segment j projects layer j's output
+// planes apl[j] ([2][M][K], hi/lo `a_pstride` apart) with layer j+1's W_ih
+// planes wpl[j].  ga.bias/C/wprogress/wncta/wxready are filled per segment.
+inline int gemm_planes_wave(const __nv_bfloat16* const* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
+                            const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
+  DynMaps mp;
+  int rc = 0;
+  for (int j = 0; j < ga.nseg && !rc; ++j) {
+    rc = make_map3(&mp.a[j], apl[j], ga.K, ga.M, 2, GBM, err, a_pstride);
+    if (!rc) rc = make_map3(&mp.b[j], wpl[j], ga.K, ga.N, 2, 256, err);
+  }
+  if (rc) return rc;
+  if ((rc = gemm_dyn_preload(err))) return rc;
+  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, ga);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("gemm_xproj_dyn (wave) launch: ") + cudaGetErrorString(e);
     return 2;
   }
   ++g_launch_count;

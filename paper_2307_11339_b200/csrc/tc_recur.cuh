@@ -149,11 +149,12 @@ __device__ __forceinline__ uint16_t h_operand(float h) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(h));
 }
 
+// The kernel body: one row-block cluster `cl` of one recurrence (a layer,
+// both directions).  recur_tc_kernel runs one layer per launch;
+// recur_tc_wave_kernel runs several unidirectional layers side by side.
 template <int G, int NPL, int CELLS, int NSW>
-__global__ void __launch_bounds__(kRecurThreads + 32, 1)
-    recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
-                    const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+__device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUtensorMap& tmW1, const CUtensorMap& tmH,
+                                              const TcRecurArgs& a, const int cl, uint8_t* smem_raw) {
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 atoms need 1024-B alignment
   signal_started(a);
@@ -179,7 +180,6 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = (int)ptx::cluster_rank();
-  const int cl = blockIdx.x / S;          // cluster index
   const int d = cl / RB;
   const int rb = cl % RB;
   const CUtensorMap* tmW = d == 0 ? &tmW0 : &tmW1;
@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
       }
     }
     if (e == 128) HS_TRACE(4);
-    if (e == kEpiThreads - 32 && !last) wait_xready(a, d == 0 ? s + 1 : T - 2 - s);  // next step's XP (see wait_xready)
+    if (e == kEpiThreads - 32 && !last) {  // next step's XP (see wait_xready)
+      HS_TRACE(7);
+      wait_xready(a, d == 0 ? s + 1 : T - 2 - s);
+      HS_TRACE(9);
+    }
     ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units are in my shared memory
     if (e == 0 && !last)  // next phase: the peers' bulk copies of step s+1
       ptx::mbar_arrive_expect_tx(red_full, (uint32_t)((S - 1) * region_floats * 4));
@@ -476,6 +480,26 @@ __global__ void __launch_bounds__(kRecurThreads + 32, 1)
     ptx::tmem_dealloc(tmem, tcols);
   }
 }
+
+template <int G, int NPL, int CELLS, int NSW>
+__global__ void __launch_bounds__(kRecurThreads + 32, 1)
+    recur_tc_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
+                    const __grid_constant__ CUtensorMap tmH, const TcRecurArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  recur_tc_body<G, NPL, CELLS, NSW>(tmW0, tmW1, tmH, a, (int)(blockIdx.x / a.S), smem_raw);
+}
+
+// Per-layer arguments of the single-GPU layer wavefront (tc_wave.cuh).
+constexpr int kMaxWave = 8;
+struct WaveMaps {
+  CUtensorMap w[kMaxWave];  // per layer: W_hh planes
+  CUtensorMap h[kMaxWave];  // per layer: h exchange planes
+};
+struct TcWaveArgs {
+  TcRecurArgs layer[kMaxWave];  // D = 1 each
+  int L;
+  int RB;  // row-block clusters per layer
+};
 
 }  // namespace tc
 }  // namespace hs
