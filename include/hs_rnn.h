@@ -99,7 +99,8 @@ int hs_rnn_resolve_algo(const hs_rnn_desc* desc, int32_t* algo);
  * (0 = W_hh resident in shared memory, > 0 = streamed from L2 every step),
  * [3] batch slices, [4] 1 if the small-shape cluster kernel runs, [5] 1 if the
  * layers run as one single-GPU layer wavefront (every layer's recurrence and
- * input projection in one launch; [1] is then its K-split), [6..7] 0. */
+ * input projection in one launch; [1] is then its K-split), [6] the wave's
+ * CTAs per SM (1 or 2), [7] 0. */
 int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info);
 
 /* Bytes of device workspace needed by hs_rnn_forward_packed / run_cells. */

@@ -221,15 +221,19 @@ struct WsLayout {
 // Recurrence K-split of the wave for this shape (static device limits), 0 = the
 // layers run one launch after another.  Unidirectional, unsliced, every layer's
 // W_hh slices resident on chip at once, the K1 on 256-wide tiles.
-int wave_split(const Dims& m) {
+hs::tc::WavePlan wave_split(const Dims& m, bool one_per_sm = false) {
   static const char* env = getenv("HS_WAVE");  // HS_WAVE=0: layer-by-layer schedule (A/B)
-  if (env && atoi(env) == 0) return 0;
+  static const char* env2 = getenv("HS_WAVE_2SM");  // HS_WAVE_2SM=0: one CTA per SM only (A/B)
+  if (env && atoi(env) == 0) return {};
   const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
-  if (m.D != 1 || m.L < 2 || m.L > hs::tc::kMaxWave) return 0;
-  if (!hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H, m.D, NPL)) return 0;
-  if (hs::tc::gemm_bn(m.G * m.H) != 256) return 0;
-  if (hs::tc::batch_slice(m.G, m.H, m.B, m.D, NPL) != m.B) return 0;
-  return hs::tc::choose_wave_split(m.G, m.H, m.B, m.L, NPL, m.G * m.H, hs::tc::static_cta_limit);
+  if (m.D != 1 || m.L < 2 || m.L > hs::tc::kMaxWave) return {};
+  if (!hs::tc::supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H, m.D, NPL)) return {};
+  if (hs::tc::gemm_bn(m.G * m.H) != 256) return {};
+  if (hs::tc::batch_slice(m.G, m.H, m.B, m.D, NPL) != m.B) return {};
+  const bool two_ok = !one_per_sm && !(env2 && atoi(env2) == 0);
+  return hs::tc::choose_wave(m.G, m.H, m.B, m.L, NPL, m.G * m.H, [&](int S, int per_sm) {
+    return per_sm == 2 && !two_ok ? 0 : hs::tc::static_wave_limit(S, per_sm);
+  });
 }
 
 // Per-layer buffers of the wave (offsets into the workspace).  Layer 0 and 1
@@ -242,7 +246,7 @@ struct WaveWs {
 };
 WaveWs wave_ws(const Dims& m, size_t base, size_t xproj0, size_t xproj1) {
   WaveWs w{};
-  if (!wave_split(m)) return w;
+  if (!wave_split(m).S) return w;
   const size_t TB = (size_t)m.T * m.B;
   size_t off = base;
   for (int l = 0; l < m.L; ++l) {
@@ -626,7 +630,7 @@ inline void chunk_bounds(int T, int n, int k, int* t0, int* t1) {
 // drains in time chunks behind the last layer's progress counters.
 int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const void* packed, const float* x,
                 const float* h0, const float* c0, float* y, float* hn, float* cn, void* ws, const WsLayout& wl,
-                cudaStream_t s, cudaStream_t gs, const Overlap* ov, bool chunked_in, bool xreq_ok, int wS,
+                cudaStream_t s, cudaStream_t gs, const Overlap* ov, bool chunked_in, bool xreq_ok, const hs::tc::WavePlan& wp,
                 cudaEvent_t* evs, int nev, float* layer_ms) {
   using namespace hs::tc;
   (void)x;
@@ -674,7 +678,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
   // ~11 steps; lag 1/2/3/4/6/8 M-tiles -> 3.51/1.78/1.59/1.63/1.71/1.79 ms)
   static const char* lag_env = getenv("HS_WAVE_LAG");
   ga.lag = lag_env ? atoi(lag_env) : (int)((12 * (size_t)m.B + 127) / 128);
-  const unsigned int ncta = (unsigned int)((m.H / 32) * wS);  // CTAs of one layer's recurrence
+  const unsigned int ncta = (unsigned int)((m.H / 32) * wp.S);  // CTAs of one layer's recurrence
   const __nv_bfloat16* whh[kMaxWave];
   const __nv_bfloat16* apl[kMaxSeg];
   const __nv_bfloat16* wih[kMaxSeg];
@@ -721,15 +725,15 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
   unsigned long long* trace = nullptr;
   if (trace_path) {
     trace = reinterpret_cast<unsigned long long*>(at<unsigned char>(ws, wl.tc) + tw.trace);
-    HS_CUDA(cudaMemsetAsync(trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
+    HS_CUDA(cudaMemsetAsync(trace, 0, (size_t)kTraceCtas * kTraceSteps * 16 * 8, s));
     for (int l = 0; l < m.L; ++l) wa.rec.layer[l].trace = trace;
   }
   if (nev) HS_CUDA(cudaEventRecord(evs[1], s));
-  if ((rc = launch_wave(m.G, NPL, wS, whh, wa, apl, apst, wih, ga, s, g_err)))
+  if ((rc = launch_wave(m.G, NPL, wp, whh, wa, apl, apst, wih, ga, s, g_err)))
     return fail(rc == 3 ? HS_ERR_UNSUPPORTED : HS_ERR_CUDA, "%s", g_err.c_str());
   if (nev) HS_CUDA(cudaEventRecord(evs[2], s));
   if (trace) {
-    static unsigned long long host[160 * kTraceSteps * 16];
+    static unsigned long long host[kTraceCtas * kTraceSteps * 16];
     HS_CUDA(cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s));
     HS_CUDA(cudaStreamSynchronize(s));
     FILE* f = fopen(trace_path, "wb");
@@ -808,10 +812,13 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   const int nsl = (m.B + Bs - 1) / Bs;
   const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
   // single-GPU layer wavefront (tc_wave.cuh): all layers in one cooperative launch
-  int wS = wave_split(m);
-  if (wS) {
-    const size_t wsm = wave_smem(m.G, m.H, m.B, wS, NPL);
-    if (wave_coresident(m.G, NPL, wS, wsm) / wS * wS < m.L * (m.H / 32) * wS + kWaveMinK1) wS = 0;  // co-tenant / MIG slice
+  // the static plan, re-checked against the device's occupancy (a co-tenant,
+  // MIG slice or cluster placement may fit fewer CTAs): two CTAs per SM, then one
+  WavePlan wp = wave_split(m);
+  for (int attempt = 0; wp.S && attempt < 2; ++attempt) {
+    const size_t wsm = wave_smem(m.G, m.H, m.B, wp.S, NPL, wp.per_sm);
+    if (wave_coresident(m.G, NPL, wp, wsm) / wp.S * wp.S >= m.L * (m.H / 32) * wp.S + kWaveMinK1) break;
+    wp = wp.per_sm == 2 && attempt == 0 ? wave_split(m, true) : WavePlan{};
   }
   cudaStream_t gs = nullptr;
   if (overlap && (rc = gemm_stream(&gs))) return rc;
@@ -899,7 +906,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
   }
-  if (wS) return wave_layers(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, gs, ov, chunked_in, xreq_ok, wS, evs, nev,
+  if (wp.S) return wave_layers(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, gs, ov, chunked_in, xreq_ok, wp, evs, nev,
                              layer_ms);
   float* xpb[2] = {at<float>(ws, wl.xproj), at<float>(ws, m.L > 1 ? wl.xproj2 : wl.xproj)};
   // XP streaming: each layer's K1 = full-GPU head over the first P timesteps,
@@ -971,7 +978,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     }
     static const char* trace_path = getenv("HS_RECUR_TRACE");
     a.trace = trace_path && l == 0 ? reinterpret_cast<unsigned long long*>(tcws + tw.trace) : nullptr;
-    if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)160 * kTraceSteps * 16 * 8, s));
+    if (a.trace) HS_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)kTraceCtas * kTraceSteps * 16 * 8, s));
     // one launch zeroes every per-layer counter / exchange region (h exchange
     // planes, chunk counters, XP readiness, claim + started counters, per-step
     // progress) instead of five memsets (~10 us of serial gaps per layer at c2)
@@ -1215,7 +1222,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       }
     }
     if (a.trace) {
-      static unsigned long long host[160 * kTraceSteps * 16];
+      static unsigned long long host[kTraceCtas * kTraceSteps * 16];
       HS_CUDA(cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s));
       HS_CUDA(cudaStreamSynchronize(s));
       FILE* f = fopen(trace_path, "wb");
@@ -1357,11 +1364,12 @@ int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info) {
     info[1] = hs::tc::plan_split(m.G, m.H, Bs, m.D, NPL, hs::tc::static_cta_limit, &nsw);
     info[2] = nsw;
     info[3] = Bs ? (m.B + Bs - 1) / Bs : 0;
-    const int wS = wave_split(m);
-    if (wS) {  // layer wavefront: K-split of the wave's recurrences
-      info[1] = wS;
+    const hs::tc::WavePlan wp = wave_split(m);
+    if (wp.S) {  // layer wavefront: K-split of the wave's recurrences, CTAs per SM
+      info[1] = wp.S;
       info[2] = 0;
       info[5] = 1;
+      info[6] = wp.per_sm;
     }
   } else {
     info[1] = small_cluster(m);

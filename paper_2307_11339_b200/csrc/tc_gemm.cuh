@@ -303,8 +303,11 @@ struct DynMaps {
   CUtensorMap b[kMaxSeg];  // W_ih planes per segment
 };
 
+// ST: TMA ring stages; NACC: TMEM accumulators (2 = double-buffered, 512
+// columns; 1 = 256 columns, for two CTAs per SM in the 2-CTA/SM layer wave)
+template <int ST_ = 4>
 struct GemmDSmem {
-  static constexpr int ST = 4, NQ = 16;
+  static constexpr int ST = ST_, NQ = 16;
   __nv_bfloat16 a[ST][GBM * GBK];
   __nv_bfloat16 b[ST][256 * GBK];
   uint64_t full[ST];
@@ -316,12 +319,15 @@ struct GemmDSmem {
   uint32_t tmem_base;
 };
 
-constexpr size_t gemm_d_smem_bytes() { return sizeof(GemmDSmem) + 1024; }
+template <int ST = 4>
+constexpr size_t gemm_d_smem_bytes() { return sizeof(GemmDSmem<ST>) + 1024; }
 
 // The body: also run by the K1 CTAs of the fused layer-wave kernel (tc_wave.cuh).
+template <int ST = 4, int NACC = 2>
 __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynArgs& g, uint8_t* smem_raw) {
-  constexpr int BN = 256, ST = GemmDSmem::ST, NQ = GemmDSmem::NQ;
-  GemmDSmem& sm = *reinterpret_cast<GemmDSmem*>(align1024(smem_raw));
+  constexpr int BN = 256, NQ = GemmDSmem<ST>::NQ;
+  constexpr uint32_t TCOLS = NACC * BN;
+  GemmDSmem<ST>& sm = *reinterpret_cast<GemmDSmem<ST>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool wave = g.nseg > 0;
   // k-blocks of a tile of segment sg (passes x K/64); the ring position is a
@@ -351,7 +357,7 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
     for (int q = 0; q < NQ; ++q) ptx::mbar_init(&sm.tq_full[q], 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 2) ptx::tmem_alloc<TCOLS>(&sm.tmem_base);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -417,8 +423,8 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
       for (int j = 0;; ++j) {
         const int t = next_tile(j);
         if (t < 0) break;
-        const int buf = j & 1;
-        if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);
+        const int buf = j % NACC;
+        if (j >= NACC) ptx::mbar_wait(&sm.tmem_empty[buf], ((j / NACC) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
         const int nkb = nkb_of((t % per_m) / tiles_n);
@@ -448,8 +454,8 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
       const float* __restrict__ bias = g.bias[sg];
       float* __restrict__ C = g.C[sg];
       unsigned int* xr = wave ? g.wxready[sg] : g.xready;
-      const int buf = j & 1;
-      ptx::mbar_wait(&sm.tmem_full[buf], (j >> 1) & 1);
+      const int buf = j % NACC;
+      ptx::mbar_wait(&sm.tmem_full[buf], (j / NACC) & 1);
       ptx::tc_fence_after();
       const int row = m0 + sub * 32 + lane;
 #pragma unroll 1
@@ -481,7 +487,7 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 512);
+    ptx::tmem_dealloc(tmem, TCOLS);
   }
 }
 

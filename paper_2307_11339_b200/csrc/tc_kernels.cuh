@@ -117,7 +117,7 @@ inline TcWs tc_ws_layout(int G, int H, int B, int T, int D, int I0) {
   w.xpl = off;      off += ((2 * (size_t)T * B * cols * 2) + 255) / 256 * 256;
   w.hbuf = off;     off += ((3 * (size_t)D * 2 * pad16(B) * H * 2) + 255) / 256 * 256;
   w.counters = off; off += 128 * 128;  // <= 128 chunk counters, one 128-B line each
-  w.trace = off;    off += (size_t)160 * kTraceSteps * 16 * 8;
+  w.trace = off;    off += (size_t)kTraceCtas * kTraceSteps * 16 * 8;
   w.progress = off; off += ((size_t)T * 4 + 255) / 256 * 256;  // per-step output counters (host-buffer forward)
   w.claim = off;    off += 512;  // tile claim counters of the dynamic K1 launches ([0], [32], [64]) + started ([96])
   w.xready = off;   off += (((size_t)T * B + 127) / 128 * 4 + 255) / 256 * 256;  // per-M-tile XP readiness
@@ -543,6 +543,8 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   int nsw = 0;
   static const char* force_sw = getenv("HS_FORCE_STREAM");  // experiments: stream W even if it fits
   int S = force_sw ? 0 : choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
+  static const char* force_s0 = getenv("HS_FORCE_S");  // experiments: cap the K-split
+  if (S && force_s0 && atoi(force_s0) > 0 && atoi(force_s0) < S) S = atoi(force_s0);
   if (!S) {
     nsw_try = kSW;
     S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);

@@ -65,11 +65,43 @@ __device__ __forceinline__ void wait_xready(const TcRecurArgs& a, int tt) {
   const int lo = (tt * a.Bst) / 128, hi = (tt * a.Bst + a.Bst - 1) / 128;
   for (int mt = lo; mt <= hi; ++mt) wait_geq(a.xready + mt, a.xready_target, kWatchRecurXready);
 }
+constexpr int kCtrStrideWords = 32;  // chunk readiness counters: one 128-B line each
+
+// The h_{t-1} all-gather of one step: lane c of the producer warp polls the
+// readiness counter of chunk c of this CTA's K-slice and, once it is
+// published, issues that chunk's TMA load itself (`issue(c)`).  All chunks are
+// polled in one round trip — polling them one after another from one lane
+// cost a serial L2 round trip per chunk (c3 at S=2, 4 chunks: 1.5 us of the
+// 5.1 us step; c2's 4 chunks: 1.2 us).  The MMA warp still consumes the
+// chunks in order, so the accumulation order is unchanged.  Whole warp.
+template <typename Issue>
+__device__ __forceinline__ void poll_chunks(const unsigned int* in_counter, int nch, unsigned int target, Issue&& issue) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int all = nch >= 32 ? 0xffffffffu : (1u << nch) - 1u;
+  unsigned int done = 0u;
+  Spin sp;
+  while (done != all) {
+    bool ok = false;
+    if (lane < nch && !((done >> lane) & 1u)) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(in_counter + lane * kCtrStrideWords) : "memory");
+      if (v >= target) {
+        ok = true;
+        issue(lane);
+      }
+    }
+    const unsigned int ready = __ballot_sync(0xffffffffu, ok);
+    if (!ready) sp.tick(kWatchRecurChunk);
+    done |= ready;
+  }
+}
+
 __device__ __forceinline__ void signal_started(const TcRecurArgs& a) {
   if (a.started && threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.started) : "memory");
 }
 
 constexpr int kTraceSteps = 64;
+constexpr int kTraceCtas = 320;  // CTAs with a trace slot (the 2-CTA/SM wave runs up to 296)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -78,7 +110,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 #define HS_TRACE(phase)                                                                          \
   do {                                                                                           \
-    if (a.trace && s < kTraceSteps)                                                              \
+    if (a.trace && s < kTraceSteps && blockIdx.x < kTraceCtas)                                   \
       a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 16 + (phase)] = globaltimer();             \
   } while (0)
 
@@ -188,7 +220,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   const uint32_t tcols = Npad <= 32 ? 32 : Npad <= 64 ? 64 : Npad <= 128 ? 128 : 256;
   // readiness counters, one per 64-unit chunk of h (= 2 row blocks = 2S producer
   // CTAs), each on its own 128-B line
-  constexpr int kCtrStride = 32;
+  constexpr int kCtrStride = kCtrStrideWords;
   const int nchunk_all = H / 64;
   unsigned int* my_counter = a.counters + (d * nchunk_all + (rb * 32) / 64) * kCtrStride;
   const unsigned int* in_counter = a.counters + (d * nchunk_all + (q * KS) / 64) * kCtrStride;
@@ -306,18 +338,15 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
     const int buf_in = s % 3, buf_out = (s + 1) % 3;
     const bool last = s == T - 1;
     if (warp == 0) {
-      if (lane == 0) {
-        HS_TRACE(0);
-        const unsigned int target = per_round * (unsigned int)(s + 1);
-        for (int c = 0; c < nch; ++c) {
-          wait_geq(in_counter + c * kCtrStride, target, kWatchRecurChunk);
-          if (c == 0) HS_TRACE(1);
-          if (c == nch - 1) HS_TRACE(12);
-          ptx::fence_proxy_async_global();
-          ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Npad * 128));
-          ptx::tma_load_3d(sH + (size_t)c * Npad * 64, &tmH, &h_full[c], q * KS + c * 64, 0, buf_in * D + d);
-        }
-      }
+      if (lane == 0) HS_TRACE(0);
+      poll_chunks(in_counter, nch, per_round * (unsigned int)(s + 1), [&](int c) {
+        if (c == 0) HS_TRACE(1);
+        if (c == nch - 1) HS_TRACE(12);
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Npad * 128));
+        ptx::tma_load_3d(sH + (size_t)c * Npad * 64, &tmH, &h_full[c], q * KS + c * 64, 0, buf_in * D + d);
+        if (c == nch - 1) HS_TRACE(13);
+      });
       __syncwarp();
     } else if (NSW && warp == 8) {
       // keep the W ring NSW items ahead: this step's chunks, then the next step's first NSW
@@ -327,7 +356,6 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       if (ptx::elect_one()) {
         if (NSW == 0 && s == 0) ptx::mbar_wait(w_full, 0);
         if (s > 0) ptx::mbar_wait(tmem_free, (s - 1) & 1);  // every warp drained step s-1
-        HS_TRACE(13);
         for (int c = 0; c < nch; ++c) {
           const int gi = s * nch + c, wslot = NSW ? gi % NSW : 0;
           if (NSW) ptx::mbar_wait(&wfull[wslot], (gi / NSW) & 1);

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256, 1)
   const int rstride = Np + 4;
   const uint32_t tcols_g = Np <= 32 ? 32 : Np <= 64 ? 64 : 128;
   const uint32_t tcols = 2 * tcols_g;
-  constexpr int kCtrStride = 32;
+  constexpr int kCtrStride = kCtrStrideWords;
   const int nchunk_all = H / 64;
   unsigned int* ctr_g = a.counters + (size_t)grp * D * nchunk_all * kCtrStride;
   unsigned int* my_counter = ctr_g + (d * nchunk_all + (rb * 32) / 64) * kCtrStride;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256, 1)
     const int t = d == 0 ? s : T - 1 - s;
     const int buf_in = s % 3, buf_out = (s + 1) % 3;
     const bool last = s == T - 1;
-    if (sub == 0) {  // producer of this group
+    if (sub == 0) {  // producer of this group (whole warp: lane-parallel chunk polls)
       if (lane == 0) {
         if (grp == 0) HS_TRACE(0);
         if (s == 0 && grp == 1 && a.group_offset_ns) {  // start group 1 out of phase
@@ -205,17 +205,15 @@ __global__ void __launch_bounds__(256, 1)
           while (globaltimer() - t0 < a.group_offset_ns) {
           }
         }
-        const unsigned int target = per_round * (unsigned int)(s + 1);
-        for (int c = 0; c < nch; ++c) {
-          wait_geq(in_counter + c * kCtrStride, target, kWatchRecurChunk);
-          if (grp == 0 && c == 0) HS_TRACE(1);
-          if (grp == 0 && c == nch - 1) HS_TRACE(12);
-          ptx::fence_proxy_async_global();
-          ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Np * 128));
-          ptx::tma_load_3d(sH + (size_t)c * Np * 64, &tmH, &h_full[c], q * KS + c * 64, 0,
-                           (buf_in * D + d) * kNG + grp);
-        }
       }
+      __syncwarp();
+      poll_chunks(in_counter, nch, per_round * (unsigned int)(s + 1), [&](int c) {
+        if (grp == 0 && c == 0) HS_TRACE(1);
+        if (grp == 0 && c == nch - 1) HS_TRACE(12);
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive_expect_tx(&h_full[c], (uint32_t)(Np * 128));
+        ptx::tma_load_3d(sH + (size_t)c * Np * 64, &tmH, &h_full[c], q * KS + c * 64, 0, (buf_in * D + d) * kNG + grp);
+      });
       __syncwarp();
     } else if (sub == 1) {  // MMA issuer of this group
       if (ptx::elect_one()) {

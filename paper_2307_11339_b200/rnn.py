@@ -278,7 +278,7 @@ class RNNExecutor:
         _check(self.lib, "hs_rnn_plan", self.lib.hs_rnn_plan(ctypes.byref(self.desc), info))
         return {"algo": ALGO_NAMES[info[0]], "cluster": info[1], "w_ring": info[2], "batch_slices": info[3],
                 "small_kernel": bool(info[4]), "w_hh_resident": info[0] == 2 and info[2] == 0,
-                "layer_wave": bool(info[5])}
+                "layer_wave": bool(info[5]), "wave_ctas_per_sm": int(info[6])}
 
     def last_launch_count(self) -> int:
         """Kernels the library launched in the last forward call on this

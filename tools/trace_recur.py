@@ -26,7 +26,7 @@ x = make_input(spec).cuda()
 for _ in range(3):
     ex.forward(x)
 torch.cuda.synchronize()
-tr = np.fromfile(out, dtype=np.uint64).reshape(160, 64, 16).astype(np.int64)
+tr = np.fromfile(out, dtype=np.uint64).reshape(320, 64, 16).astype(np.int64)
 used = tr[:, :, 0] > 0
 ncta = int(used.any(axis=1).sum())
 tr = tr[:ncta]

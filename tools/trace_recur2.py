@@ -19,7 +19,7 @@ x = make_input(spec).cuda()
 for _ in range(3):
     ex.forward(x)
 torch.cuda.synchronize()
-tr = np.fromfile(out, dtype=np.uint64).reshape(160, 64, 16).astype(np.int64)[:128]
+tr = np.fromfile(out, dtype=np.uint64).reshape(320, 64, 16).astype(np.int64)[:128]
 T0, T1 = 2, 60
 ph = lambda i: tr[:, T0:T1, i]
 med = lambda v: np.median(v) / 1e3

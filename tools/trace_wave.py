@@ -32,7 +32,7 @@ x = make_input(spec).cuda()
 for _ in range(3):
     ex.forward(x)
 torch.cuda.synchronize()
-tr = np.fromfile(out, dtype=np.uint64).reshape(160, 64, 16).astype(np.int64)
+tr = np.fromfile(out, dtype=np.uint64).reshape(320, 64, 16).astype(np.int64)
 S, L, RB = plan["cluster"], spec.layers, spec.hidden // 32
 per = RB * S
 t0 = tr[:per, 0, 0].min()
@@ -50,7 +50,8 @@ for l in range(L):
 rows = [
     ("producer: top -> chunk0 ready", 0, 1),
     ("producer: chunk0 ready -> last ready", 1, 12),
-    ("mma: last ready -> last landed", 12, 14),
+    ("producer: last ready -> its TMA issued", 12, 13),
+    ("mma: last TMA issued -> last landed", 13, 14),
     ("mma: last landed -> commit issued", 14, 2),
     ("epi: commit -> acc_full seen", 2, 3),
     ("epi: tmem ld + partial staging", 3, 4),
