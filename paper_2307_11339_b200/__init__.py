@@ -64,6 +64,7 @@ from .planner import (
     save_plan,
     select_devices,
     sweep_alpha,
+    sweep_csv,
     sweep_core_counts,
     topo_sort_bfs,
     topo_sort_dfs,
@@ -84,7 +85,7 @@ __all__ = [
     "comm_time", "crossing", "check_compatible", "load_profile", "save_profile",
     # planner
     "Order", "Plan", "PlanFormatError", "CoreCountPoint", "AlphaPoint", "topo_sort_bfs",
-    "topo_sort_dfs", "topo_sort_hybrid", "select_devices", "sweep_core_counts", "sweep_alpha",
+    "topo_sort_dfs", "topo_sort_hybrid", "select_devices", "sweep_core_counts", "sweep_alpha", "sweep_csv",
     "memory_optimal_alpha", "latency_optimal_plan", "reduce_movements", "check_plan",
     "crossing_count", "load_plan", "save_plan",
     # evaluation

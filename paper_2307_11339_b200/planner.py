@@ -302,6 +302,20 @@ def sweep_alpha(
     return out
 
 
+def sweep_csv(graph: "Graph", cm: CostModel, alphas="0:1:0.1", io_transfers: bool = False) -> str:
+    """The frontier as the reference's ``sweep.csv`` text (cli.py:259-306):
+    ``kind,alpha,latency_ms,gpu_memory_mb,k_star`` — one ``plan`` row per alpha,
+    then the all-GPU and all-CPU baselines; floats written with ``repr``."""
+    lines = ["kind,alpha,latency_ms,gpu_memory_mb,k_star"]
+    for p in sweep_alpha(graph, cm, alphas, io_transfers):
+        lines.append(f"plan,{p.alpha!r},{p.latency!r},{p.gpu_memory!r},{p.k_star}")
+    gpu_plan, cpu_plan = engine.baseline_plans(graph, cm, io_transfers)
+    for kind, plan, k in (("baseline-gpu", gpu_plan, 0), ("baseline-cpu", cpu_plan, cpu_plan.k_star)):
+        ev = engine.evaluate(graph, cm, plan, io_transfers)
+        lines.append(f"{kind},,{ev.latency!r},{ev.gpu_memory!r},{k}")
+    return "\n".join(lines) + "\n"
+
+
 def memory_optimal_alpha(
     graph: "Graph",
     cm: CostModel,

@@ -37,6 +37,7 @@ def corpus_specs():
         for preset in ("cpu-comparable", "gpu-dominant", "comm-heavy"):
             specs.append(("lstm", [L, T], preset, 0))
     specs.append(("lstm", [4, 256], "cpu-comparable", 0))
+    specs.append(("lstm", [8, 512], "cpu-comparable", 0))  # c4 grid (n = 4096)
     rng = np.random.default_rng(2026)
     for _ in range(40):
         n = int(rng.integers(2, 40))
