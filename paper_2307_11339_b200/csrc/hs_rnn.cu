@@ -969,6 +969,10 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     a.ypl = last ? nullptr : xpl;
     a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
+    // L2 eviction policies for the W-streaming variant (tc_recur.cuh
+    // kL2Hint*); HS_L2_HINTS=<bits> overrides (A/B), 0 = none
+    static const char* l2h_env = getenv("HS_L2_HINTS");
+    a.l2_hints = l2h_env ? atoi(l2h_env) : kL2HintW | kL2HintStream;
     // HS_TEST_STALL=1 (watchdog test only): layer 0 waits for K1 tiles that
     // never come, so its first XP poll can only end through the watchdog
     static const bool test_stall = getenv("HS_TEST_STALL") != nullptr;

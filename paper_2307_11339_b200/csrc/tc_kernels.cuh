@@ -457,10 +457,14 @@ inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
   return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
 }
 
-// persistent recurrences launch cooperatively (HS_COOP=0: plain cluster launch, A/B only)
+// persistent recurrences launch cooperatively (HS_COOP=0: plain cluster launch,
+// A/B only).  Nsight Compute fails cooperative cluster launches with
+// LaunchFailed; it replays one kernel at a time, so the occupancy check
+// before every launch already guarantees the whole grid is resident there.
 inline bool coop_launch() {
   static const char* env = getenv("HS_COOP");
-  return !(env && atoi(env) == 0);
+  static const bool ncu = getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR");
+  return !(env && atoi(env) == 0) && !ncu;
 }
 
 template <int G, int NPL, int CELLS, int NSW>

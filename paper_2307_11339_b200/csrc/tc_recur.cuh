@@ -53,7 +53,12 @@ struct TcRecurArgs {
   const unsigned int* xready;
   unsigned int xready_target;
   unsigned int* started;        // optional: +1 per CTA once resident (gates the side-stream K1)
+  // L2 eviction policies (kL2Hint*): the streamed W_hh ring evict_last, the
+  // read-once xproj rows and the y stores evict_first, so the W_hh bytes the
+  // streaming variant re-reads every step stay in L2 (c4: 64 MiB of 126 MB)
+  int l2_hints;
 };
+constexpr int kL2HintW = 1, kL2HintStream = 2;
 
 // Block until the K1 tiles holding timestep tt's rows of xproj are stored.
 // In the time loop ONE lane of an epilogue-only warp does this for step s+1
@@ -262,13 +267,21 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   // Ring item gi = s*nch + c holds chunk c (the same weights every step).
   const int total_items = T * nch;
   int w_next = 0;  // next ring item to load (warp 8 lane 0)
+  const uint64_t pol_w = ptx::policy_evict_last();
+  const uint64_t pol_s = ptx::policy_evict_first();
+  const bool hint_s = (a.l2_hints & kL2HintStream) != 0;
   auto w_produce_until = [&](int last_item) {
     for (; w_next <= last_item && w_next < total_items; ++w_next) {
       const int slot = w_next % NSW, c = w_next % nch;
       if (w_next >= NSW) ptx::mbar_wait(&wempty[slot], ((w_next / NSW) - 1) & 1);
       ptx::mbar_arrive_expect_tx(&wfull[slot], (uint32_t)(NPL * 128 * 128));
-      for (int p = 0; p < NPL; ++p)
-        ptx::tma_load_3d(sW + ((size_t)slot * NPL + p) * 128 * 64, tmW, &wfull[slot], q * KS + c * 64, rb * 128, p);
+      for (int p = 0; p < NPL; ++p) {
+        if (a.l2_hints & kL2HintW)
+          ptx::tma_load_3d_hint(sW + ((size_t)slot * NPL + p) * 128 * 64, tmW, &wfull[slot], q * KS + c * 64, rb * 128,
+                                p, pol_w);
+        else
+          ptx::tma_load_3d(sW + ((size_t)slot * NPL + p) * 128 * 64, tmW, &wfull[slot], q * KS + c * 64, rb * 128, p);
+      }
     }
   };
 
@@ -298,7 +311,9 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
     for (int k = 0; k < CELLS; ++k) {
       const int b = b0 + k * bstep;
 #pragma unroll
-      for (int g = 0; g < G; ++g) xq[k][g] = b < B ? __ldcg(xp + (size_t)b * GH + g * H) : 0.f;  // may be written by a running K1
+      for (int g = 0; g < G; ++g) xq[k][g] = b < B ? (hint_s ? ptx::ldcg_hint(xp + (size_t)b * GH + g * H, pol_s)
+                                                                 : __ldcg(xp + (size_t)b * GH + g * H))
+                                   : 0.f;  // may be written by a running K1
     }
   };
 #pragma unroll
@@ -482,7 +497,10 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       if (b >= B) continue;
       const float hv = h_reg[k];
       const size_t yidx = ((size_t)t * a.Bst + b) * D * H + (size_t)d * H + unit;
-      if (a.y) a.y[yidx] = hv;
+      if (a.y) {
+        if (hint_s) ptx::st_hint(a.y + yidx, hv, pol_s);
+        else a.y[yidx] = hv;
+      }
       if (a.ypl) {
         __nv_bfloat16 hi, lo;
         ptx::split_bf16(hv, hi, lo);

@@ -223,7 +223,7 @@ inline int launch_wave(int G, int NPL, const WavePlan& p, const __nv_bfloat16* c
     attr[1].id = cudaLaunchAttributeCooperative;  // the whole grid resident: waits between CTAs never starve
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = coop_launch() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, rm, wa, gm, ga);
     if (e != cudaSuccess) {
       err = std::string("wave_fused_kernel launch: ") + cudaGetErrorString(e);

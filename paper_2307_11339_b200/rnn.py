@@ -247,9 +247,12 @@ class RNNExecutor:
             self.algo = ALGO_NAMES[a.value]
             n = ctypes.c_size_t()
             _check(self.lib, "hs_rnn_packed_size", self.lib.hs_rnn_packed_size(ctypes.byref(self.desc), ctypes.byref(n)))
-            self.packed = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
+            self._packed_n = max(n.value, 1)
+            self.packed = torch.empty(self._packed_n, dtype=torch.uint8, device=self.device)
+            self._packed_host = None
             _check(self.lib, "hs_rnn_workspace", self.lib.hs_rnn_workspace(ctypes.byref(self.desc), ctypes.byref(n)))
-            self.workspace = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
+            self._ws_n = max(n.value, 1)
+            self.workspace = torch.empty(self._ws_n, dtype=torch.uint8, device=self.device)
             self.weights = [
                 {k: v.to(self.device, torch.float32).contiguous() for k, v in w.items()} for w in weights
             ]
@@ -271,6 +274,54 @@ class RNNExecutor:
                     ctypes.byref(self.desc), *arrs, self.packed.data_ptr(), self.packed.numel(), stream.cuda_stream
                 ),
             )
+
+    # ---------------------------------------------------------------- residency
+    # A serving process keeps more models than fit in HBM (servingsim.py:1-8):
+    # the packed weights have a pinned host master copy, and a non-resident
+    # executor holds no device memory.  Loading is one H2D copy of the packed
+    # buffer (weights are immutable, so eviction needs no copy back).
+
+    @property
+    def resident(self) -> bool:
+        return self.packed is not None
+
+    def packed_bytes(self) -> int:
+        return int(self._packed_n)
+
+    def workspace_bytes(self) -> int:
+        return int(self._ws_n)
+
+    def offload(self) -> None:
+        """Release this model's device memory (packed weights, workspace and
+        the fp32 weight copies); a pinned host copy of the packed buffer is
+        kept for :meth:`load`."""
+        if not self.resident:
+            return
+        if self._packed_host is None:
+            self._packed_host = torch.empty(self.packed.numel(), dtype=torch.uint8).pin_memory()
+            self._packed_host.copy_(self.packed)
+        if self.weights and self.weights[0]["w_ih"].device.type != "cpu":
+            self.weights = [{k: v.cpu() for k, v in w.items()} for w in self.weights]
+        self.packed = None
+        self.workspace = None
+
+    def load(self, stream=None) -> None:
+        """Make the model resident again: allocate its device buffers and
+        upload the packed weights (asynchronous on ``stream``, default the
+        current stream; later work on that stream is ordered after it)."""
+        if self.resident:
+            return
+        with torch.cuda.device(self.device):
+            st = stream if stream is not None else torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(st):
+                packed = torch.empty(self._packed_n, dtype=torch.uint8, device=self.device)
+                packed.copy_(self._packed_host, non_blocking=True)
+                self.workspace = torch.empty(self._ws_n, dtype=torch.uint8, device=self.device)
+            self.packed = packed
+
+    def _require_resident(self):
+        if not self.resident:
+            raise RuntimeError("model is not resident on the device (offloaded); call load() first")
 
     def plan(self) -> dict:
         """The library's execution plan for this model (``hs_rnn_plan``)."""
@@ -309,6 +360,7 @@ class RNNExecutor:
     def forward(self, x: torch.Tensor, h0=None, c0=None, out=None, layer_ms: bool = False):
         """Run the DAG on device tensors.  Returns ``(y, h_n, c_n)`` (c_n None
         for GRU), plus per-layer [gemm_ms, recurrent_ms] when ``layer_ms``."""
+        self._require_resident()
         s = self.spec
         if x.device != self.device or x.dtype != torch.float32 or not x.is_contiguous():
             raise ValueError("x must be a contiguous float32 tensor on the executor's device")
@@ -350,6 +402,7 @@ class RNNExecutor:
         host ``(y, h_n, c_n)``; work is complete when the current stream is.
         ``upload_chunks``: time chunks x is uploaded in (0 = library default);
         1 suits request streams, where the upload overlaps the previous request."""
+        self._require_resident()
         s = self.spec
         for name, t in (("x", x_host), ("h0", h0), ("c0", c0)):
             if t is not None and (t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous()):
@@ -395,6 +448,7 @@ class RNNExecutor:
 
     def run_cells(self, ld: int, t0: int, t1: int, inp, out, h_prev, c_prev, h_last, c_last):
         """Steps ``t0..t1-1`` (processing order) of layer-direction ``ld``."""
+        self._require_resident()
         ptr = lambda t: t.data_ptr() if t is not None else None
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device)
