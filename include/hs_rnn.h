@@ -15,8 +15,10 @@
  *   engine.simulate, per-node NodeSpan           hs_rnn_run_cells (one layer-direction,
  *                                                a contiguous run of timesteps = a GPU
  *                                                segment of a hybrid plan)
- *   costmodel.synth_profile -> W[:,0]            hs_rnn_profile (CUDA-event times per
- *                                                layer-direction kernel)
+ *   costmodel.synth_profile -> W[:,0]            hs_rnn_profile_cells (per-cell ms from
+ *                                                per-step %globaltimer stamps), and the
+ *                                                per-layer CUDA-event times of
+ *                                                hs_rnn_forward_packed(..., layer_ms)
  *
  * Conventions: every pointer argument that names a tensor is a DEVICE pointer
  * allocated by the caller (PyTorch); the library never allocates or frees
@@ -125,6 +127,22 @@ int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed,
                           void* workspace, size_t ws_bytes, void* stream,
                           float* layer_ms);
 
+/* Per-cell GPU cost of the whole-DAG forward (the measured replacement of
+ * costmodel.synth_profile's W[:, 0], costmodel.py:176-221, which the planner
+ * reads per node, costmodel.py:141-150).  Runs hs_rnn_forward_packed once with
+ * per-step %globaltimer stamps in each layer-direction's recurrence and
+ * synchronizes.  cell_ms [layers*dirs*T] is indexed like the cell grid's nodes,
+ * (l*dirs + d)*T + t (graph.gen_lstm_grid / gen_bilstm_grid): each cell gets
+ * its measured step period, scaled so that all cells sum to the measured
+ * forward (CUDA events; also returned in *forward_ms when non-NULL).  Paths
+ * without stamps (SIMT, small-shape cluster kernel) get the mean period.
+ * Needs the workspace of hs_rnn_workspace. */
+int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed,
+                         const void* x, const void* h0, const void* c0,
+                         void* y, void* hn, void* cn,
+                         void* workspace, size_t ws_bytes, void* stream,
+                         float* cell_ms, float* forward_ms);
+
 /* End-to-end forward on HOST buffers (the request path; pinned host memory
  * gives asynchronous copies).  x_host [T,B,I], h0_host/c0_host
  * [L*D,B,H] or NULL, outputs y_host [T,B,D*H], hn_host/cn_host [L*D,B,H].
@@ -153,7 +171,10 @@ int hs_rnn_forward(const hs_rnn_desc* desc, const void* x,
                    void* workspace, size_t ws_bytes, void* stream);
 
 /* One GPU segment of a plan: timesteps t0..t1-1 (in the direction's own
- * processing order) of layer-direction `ld`.  `in` is that layer's input
+ * processing order) of layer-direction `ld`.  On the tensor-core path the
+ * segment runs the fused forward's kernels (split + K1 GEMM over the
+ * segment's rows, then one recurrence launch of this layer-direction); shapes
+ * the tensor-core path does not cover run the SIMT kernels.  `in` is that layer's input
  * [T, B, I_l], `out` its output [T, B, dirs*H] (columns d*H..d*H+H-1 are
  * written), `h_prev`/`c_prev` [B, H] the state entering step t0 and
  * `h_last`/`c_last` [B, H] receive the state after step t1-1.  `c_prev` and

@@ -14,6 +14,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hs_rnn.h"
 #include "cluster_small.cuh"
@@ -214,8 +215,12 @@ int pack_layout(const Dims& m, PackLayout* p) {
 
 // ----------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t xproj, xproj2, act0, act1, cst, zeros, barrier, tc, wave, total;
+  size_t xproj, xproj2, act0, act1, cst, zeros, barrier, tc, wave, stamps, total;
 };
+// hs_rnn_profile_cells: per-step %globaltimer stamps of every layer-direction
+// ([L*D][T+1], workspace region WsLayout::stamps) for the forward in flight on
+// this thread; nullptr otherwise
+thread_local unsigned long long* g_stamps = nullptr;
 
 // ---- single-GPU layer wavefront (tc_wave.cuh): feasibility and workspace
 // Recurrence K-split of the wave for this shape (static device limits), 0 = the
@@ -284,7 +289,8 @@ WsLayout ws_layout(const Dims& m) {
   w.zeros = off;   off = align_up(off + sizeof(float) * m.D * m.B * m.H);
   w.barrier = off; off = align_up(off + 256);
   w.tc = off;      off = align_up(off + hs::tc::workspace_bytes(m.G, m.H, m.B, m.T, m.D, m.in_size(0)));
-  w.wave = off;    off += wave_ws(m, off, w.xproj, w.xproj2).bytes;
+  w.wave = off;    off = align_up(off + wave_ws(m, off, w.xproj, w.xproj2).bytes);
+  w.stamps = off;  off += sizeof(unsigned long long) * m.L * m.D * (m.T + 1);
   w.total = off;
   return w;
 }
@@ -704,6 +710,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
     a.hbuf = at<uint16_t>(ws, ww.hbuf[l]);
     a.counters = at<unsigned int>(ws, ww.counters[l]);
     a.progress = at<unsigned int>(ws, ww.progress[l]);
+    a.stamps = g_stamps ? g_stamps + (size_t)l * (m.T + 1) : nullptr;
     if (l >= seg0) {
       const int j = l - seg0;
       a.xready = at<unsigned int>(ws, ww.xready[l]);
@@ -969,6 +976,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     a.ypl = last ? nullptr : xpl;
     a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
+    a.stamps = g_stamps ? g_stamps + (size_t)l * m.D * (m.T + 1) : nullptr;
     // L2 eviction policies for the W-streaming variant (tc_recur.cuh
     // kL2Hint*); HS_L2_HINTS=<bits> overrides (A/B), 0 = none
     static const char* l2h_env = getenv("HS_L2_HINTS");
@@ -1128,6 +1136,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         sa.ypl = a.ypl ? a.ypl + (size_t)b0 * m.D * m.H : nullptr;
         sa.progress = nullptr;
         sa.trace = nullptr;
+        if (j) sa.stamps = nullptr;  // slice 0's steps stand for the layer's (profile_cells rescales)
         if (j) {
           HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
           HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
@@ -1332,6 +1341,69 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
 
 }  // namespace
 
+// One GPU segment of a plan on the tensor-core path (hs_rnn_run_cells):
+// the segment's input rows go through the split + K1 GEMM, then ONE
+// recurrence launch of the layer-direction alone runs steps t0..t1-1 from
+// h_prev/c_prev (TcRecurArgs s_base / rev / ycols), i.e. the same kernels the
+// fused forward runs, so hybrid plans execute what profile_ops measured.
+// Returns -1 when the shape needs the SIMT segment path (no tensor-core
+// support, or a batch too large for one co-resident recurrence).
+int tc_run_cells(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const void* packed, int ld, int t0, int t1,
+                 const float* in, float* out, const float* h_prev, const float* c_prev, float* h_last, float* c_last,
+                 void* ws, const WsLayout& wl, cudaStream_t s) {
+  using namespace hs::tc;
+  const int NPL = m.dtype == HS_DTYPE_BF16 ? 1 : 2;
+  if (!supports(m.G, m.H, m.B, m.in_size(0), m.D * m.H, m.D, NPL)) return -1;
+  if (batch_slice(m.G, m.H, m.B, m.D, NPL) != m.B) return -1;
+  const int l = ld / m.D, d = ld % m.D, Il = m.in_size(l);
+  const int GH = m.G * m.H;
+  const LayerPack& lp = pl.ld[ld];
+  const TcWs tw = tc_ws_layout(m.G, m.H, m.B, m.T, m.D, m.I);
+  unsigned char* tcws = at<unsigned char>(ws, wl.tc);
+  __nv_bfloat16* xpl = reinterpret_cast<__nv_bfloat16*>(tcws + tw.xpl);
+  // input rows of the processed timesteps: [tlo, thi) (reverse direction: mirrored)
+  const int tlo = d == 0 ? t0 : m.T - t1, thi = d == 0 ? t1 : m.T - t0;
+  const size_t rows = (size_t)(thi - tlo) * m.B;
+  float* xp = at<float>(ws, wl.xproj) + (size_t)d * m.T * m.B * GH;
+  const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
+  int rc;
+  if ((rc = split_planes(in + (size_t)tlo * m.B * Il, xpl, rows, Il, s, g_err))) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+  if ((rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp + (size_t)tlo * m.B * GH, (int)rows, GH, Il,
+                        NPL == 2 ? 3 : 1, s, g_err)))
+    return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+  {
+    ZeroList zl{};
+    zl.p[0] = reinterpret_cast<uint4*>(tcws + tw.hbuf);
+    zl.n16[0] = (3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2 + 15) / 16;
+    zl.p[1] = reinterpret_cast<uint4*>(tcws + tw.counters);
+    zl.n16[1] = 128 * 128 / 16;
+    zl.k = 2;
+    zero_list_kernel<<<di.sms, 256, 0, s>>>(zl);
+    HS_CUDA(cudaGetLastError());
+    ++hs::g_launch_count;
+  }
+  TcRecurArgs a{};
+  a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = t1 - t0; a.D = 1; a.Bst = m.B;
+  a.s_base = t0; a.T_full = m.T; a.rev = d; a.ycols = m.D * m.H;
+  a.xproj[0] = xp;
+  a.bias_h[0] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+  a.whh_scale[0] = whh_scales(at<unsigned char>(const_cast<void*>(packed), lp.tc), m.G, m.H, Il);
+  a.h0[0] = h_prev;
+  a.c0[0] = m.G == 4 ? c_prev : h_prev;  // GRU never reads c
+  a.hn[0] = h_last;
+  a.cn[0] = m.G == 4 ? c_last : nullptr;
+  a.y = out + (size_t)d * m.H;
+  a.hbuf = reinterpret_cast<uint16_t*>(tcws + tw.hbuf);
+  a.counters = reinterpret_cast<unsigned int*>(tcws + tw.counters);
+  a.l2_hints = kL2HintW | kL2HintStream;
+  const __nv_bfloat16* whh[2];
+  whh[0] = whh[1] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
+  rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
+  if (rc == 3) return -1;
+  if (rc) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+  return HS_OK;
+}
+
 extern "C" {
 
 int hs_abi_version(void) { return HS_RNN_ABI_VERSION; }
@@ -1463,6 +1535,84 @@ int hs_rnn_forward_packed(const hs_rnn_desc* desc, const void* packed, const voi
                       static_cast<float*>(cn), workspace, wl, static_cast<cudaStream_t>(stream), layer_ms);
 }
 
+int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed, const void* x, const void* h0, const void* c0,
+                         void* y, void* hn, void* cn, void* workspace, size_t ws_bytes, void* stream, float* cell_ms,
+                         float* forward_ms) {
+  hs::g_launch_count = 0;
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!packed || !x || !y || !hn || !workspace || !cell_ms)
+    return fail(HS_ERR_INVALID, "packed, x, y, hn, workspace and cell_ms must be non-NULL");
+  if (m.G == 4 && !cn) return fail(HS_ERR_INVALID, "LSTM needs a c_n output");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  WsLayout wl = ws_layout(m);
+  if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int LD = m.L * m.D, T = m.T;
+  const size_t nst = (size_t)LD * (T + 1);
+  unsigned long long* st = at<unsigned long long>(workspace, wl.stamps);
+  HS_CUDA(cudaMemsetAsync(st, 0, nst * sizeof(unsigned long long), s));
+  cudaEvent_t ev[2];
+  HS_CUDA(cudaEventCreate(&ev[0]));
+  HS_CUDA(cudaEventCreate(&ev[1]));
+  HS_CUDA(cudaEventRecord(ev[0], s));
+  g_stamps = st;
+  rc = forward_impl(m, algo, di, pl, packed, static_cast<const float*>(x), static_cast<const float*>(h0),
+                    static_cast<const float*>(c0), static_cast<float*>(y), static_cast<float*>(hn),
+                    static_cast<float*>(cn), workspace, wl, s, nullptr);
+  g_stamps = nullptr;
+  if (rc) return rc;
+  HS_CUDA(cudaEventRecord(ev[1], s));
+  std::vector<unsigned long long> h(nst);
+  HS_CUDA(cudaMemcpyAsync(h.data(), st, nst * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  HS_CUDA(cudaStreamSynchronize(s));
+  float fwd = 0.f;
+  HS_CUDA(cudaEventElapsedTime(&fwd, ev[0], ev[1]));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (forward_ms) *forward_ms = fwd;
+  // per-step periods of each layer-direction's chain; layer-directions whose
+  // kernel records no stamps (SIMT / small-shape paths) get the mean period.
+  // All periods are then scaled so the cells sum to the measured forward:
+  // the all-GPU plan's modelled latency stays the measured one (engine.py:
+  // 167-210 runs GPU nodes one at a time), while the split between cells
+  // follows the measured steps (pipeline fill, slower first steps)
+  std::vector<double> per((size_t)LD * T, 0.0);
+  std::vector<char> stamped(LD, 0);
+  double sum = 0.0;
+  int have = 0;
+  for (int ld = 0; ld < LD; ++ld) {
+    const unsigned long long* r = h.data() + (size_t)ld * (T + 1);
+    bool ok = true;
+    for (int i = 0; i <= T; ++i) ok = ok && r[i] != 0 && (i == 0 || r[i] >= r[i - 1]);
+    if (!ok) continue;
+    stamped[ld] = 1;
+    ++have;
+    const int d = ld % m.D;
+    for (int i = 0; i < T; ++i) {
+      const int t = d == 0 ? i : T - 1 - i;  // node (ld, t) is processing step i
+      per[(size_t)ld * T + t] = (double)(r[i + 1] - r[i]);
+      sum += per[(size_t)ld * T + t];
+    }
+  }
+  const double fill = have ? sum / ((double)have * T) : 1.0;
+  for (int ld = 0; ld < LD; ++ld) {
+    if (stamped[ld]) continue;
+    for (int t = 0; t < T; ++t) {
+      per[(size_t)ld * T + t] = fill;
+      sum += fill;
+    }
+  }
+  for (size_t i = 0; i < per.size(); ++i) cell_ms[i] = (float)(per[i] * (double)fwd / sum);
+  return HS_OK;
+}
+
 int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void* x_host, const void* h0_host,
                         const void* c0_host, void* y_host, void* hn_host, void* cn_host, void* x_dev, void* y_dev,
                         void* hn_dev, void* cn_dev, void* state_dev, void* workspace, size_t ws_bytes, void* stream) {
@@ -1554,6 +1704,16 @@ int hs_rnn_run_cells(const hs_rnn_desc* desc, const void* packed, int32_t ld, in
   WsLayout wl = ws_layout(m);
   if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  static const char* seg_env = getenv("HS_SEG_SIMT");  // HS_SEG_SIMT=1: SIMT segments (A/B)
+  if (algo == HS_ALGO_TC && !(seg_env && atoi(seg_env) == 1)) {
+    rc = tc_run_cells(m, di, pl, packed, ld, t0, t1, static_cast<const float*>(in), static_cast<float*>(out),
+                      static_cast<const float*>(h_prev), static_cast<const float*>(c_prev), static_cast<float*>(h_last),
+                      static_cast<float*>(c_last), workspace, wl, s);
+    if (rc >= 0) return rc;
+    hs::g_launch_count = 0;  // nothing was launched for a -1
+  }
   const int l = ld / m.D, d = ld % m.D;
   const LayerPack& lp = pl.ld[ld];
   // Input projection for the processed timesteps only: rows [tlo, thi) of `in`.

@@ -57,7 +57,21 @@ struct TcRecurArgs {
   // read-once xproj rows and the y stores evict_first, so the W_hh bytes the
   // streaming variant re-reads every step stay in L2 (c4: 64 MiB of 126 MB)
   int l2_hints;
+  // A segment of a layer-direction (hs_rnn_run_cells): the launch runs T
+  // steps starting at processing step s_base of a T_full-step sequence; rev
+  // = 1 walks it backwards (the reverse direction launched alone, D = 1);
+  // ycols = floats per y row (0 = D*H).  All zero = the whole layer.
+  int s_base, T_full, rev, ycols;
+  // optional per-step %globaltimer stamps of cluster 0 rank 0 of each
+  // direction: stamps[d*(T+1)] at the first step's start, stamps[d*(T+1)+s+1]
+  // when step s's h is released (hs_rnn_profile_cells)
+  unsigned long long* stamps;
 };
+// timestep (row of xproj / y) of processing step `step` of direction d
+__device__ __forceinline__ int seg_time(const TcRecurArgs& a, int d, int step) {
+  const int Tf = a.T_full ? a.T_full : a.T;
+  return ((d == 0) != (a.rev != 0)) ? a.s_base + step : Tf - 1 - a.s_base - step;
+}
 constexpr int kL2HintW = 1, kL2HintStream = 2;
 
 // Block until the K1 tiles holding timestep tt's rows of xproj are stored.
@@ -304,7 +318,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
     bias_n = a.bias_h[d][2 * H + unit];
   }
   auto load_xproj = [&](int step, bool poll) {
-    const int tt = d == 0 ? step : T - 1 - step;
+    const int tt = seg_time(a, d, step);
     if (poll) wait_xready(a, tt);
     const float* __restrict__ xp = a.xproj[d] + (size_t)tt * a.Bst * GH + unit;
 #pragma unroll
@@ -333,6 +347,8 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
   cluster_arrive();  // every CTA's barriers initialised before any remote op
   cluster_wait();
+  const bool stamper = a.stamps && rb == 0 && q == 0 && threadIdx.x == 0;
+  if (stamper) a.stamps[(size_t)d * (T + 1)] = globaltimer();
 
   // f32 mode: fp16 W hi/lo x fp16 h; bf16 mode: bf16 x bf16
   const uint32_t idesc = NPL == 2 ? idesc_f16_f32(128, Npad) : ptx::idesc_bf16_f32(128, Npad);
@@ -349,7 +365,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
                                         ((size_t)sub * UO + lane % UO) * rstride;
 
   for (int s = 0; s < T; ++s) {
-    const int t = d == 0 ? s : T - 1 - s;
+    const int t = seg_time(a, d, s);
     const int buf_in = s % 3, buf_out = (s + 1) % 3;
     const bool last = s == T - 1;
     if (warp == 0) {
@@ -436,7 +452,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
     if (e == 128) HS_TRACE(4);
     if (e == kEpiThreads - 32 && !last) {  // next step's XP (see wait_xready)
       HS_TRACE(7);
-      wait_xready(a, d == 0 ? s + 1 : T - 2 - s);
+      wait_xready(a, seg_time(a, d, s + 1));
       HS_TRACE(9);
     }
     ptx::mbar_wait_cluster(red_full, s & 1);  // all partials for my units are in my shared memory
@@ -485,6 +501,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
     __syncthreads();  // all h_t stores of this CTA issued
     if (e == 128) HS_TRACE(8);
     if (e == 0 && !last) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(my_counter) : "memory");
+    if (stamper) a.stamps[(size_t)d * (T + 1) + s + 1] = globaltimer();
     // the barrier above also ordered every thread's y stores of step s-1:
     // publish them for the overlapped device->host copy (off the critical path)
     if (a.progress && e == kEpiThreads - 32 && s > 0)
@@ -496,7 +513,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       const int b = b0 + k * bstep;
       if (b >= B) continue;
       const float hv = h_reg[k];
-      const size_t yidx = ((size_t)t * a.Bst + b) * D * H + (size_t)d * H + unit;
+      const size_t yidx = ((size_t)t * a.Bst + b) * (a.ycols ? a.ycols : D * H) + (size_t)d * H + unit;
       if (a.y) {
         if (hint_s) ptx::st_hint(a.y + yidx, hv, pol_s);
         else a.y[yidx] = hv;

@@ -184,6 +184,8 @@ __global__ void __launch_bounds__(256, 1)
   group_release(my_counter);
   cluster_arrive();  // every CTA's barriers initialised before any remote op
   cluster_wait();
+  const bool stamper = a.stamps && rb == 0 && q == 0 && threadIdx.x == 0;  // group 0's chain
+  if (stamper) a.stamps[(size_t)d * (T + 1)] = globaltimer();
 
   const uint32_t idesc = NPL == 2 ? idesc_f16_f32(128, Np) : ptx::idesc_bf16_f32(128, Np);
   const bool active = sub < G;
@@ -320,6 +322,7 @@ __global__ void __launch_bounds__(256, 1)
     if (!last) {
       ptx::fence_proxy_async_global();
       group_release(my_counter);
+      if (stamper) a.stamps[(size_t)d * (T + 1) + s + 1] = globaltimer();
       // the group barrier inside group_release also ordered the group's y stores
       // of step s-1: publish them for the overlapped K1 / device->host copy from
       // a thread off the critical path (warp 3 of the group: neither the
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(256, 1)
       if (a.progress && s > 0 && eg == 96)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.progress + s - 1) : "memory");
     }
+    if (stamper && last) a.stamps[(size_t)d * (T + 1) + T] = globaltimer();
     if (threadIdx.x == 0) HS_TRACE(10);
     // 3. off the critical path: outputs, final state, next step's XP
 #pragma unroll

@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import os
 import statistics
+import sys
 import threading
 import time
 from dataclasses import dataclass
@@ -54,6 +55,7 @@ __all__ = [
     "execute",
     "profile_ops",
     "measure_link_bandwidth",
+    "measure_link_latency",
 ]
 
 MB = float(2**20)
@@ -448,6 +450,11 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
             fail.set(exc)
 
     prev_threads = torch.get_num_threads()
+    # cells hand off between worker threads at every crossing: a short GIL
+    # switch interval (default 5 ms) keeps a woken waiter from queueing behind
+    # a running worker for a whole interval
+    prev_switch = sys.getswitchinterval()
+    sys.setswitchinterval(5e-5)
     threads = [threading.Thread(target=host_worker, args=(c, q), daemon=True) for c, q in sorted(sched.host.items())]
     if uses_gpu:
         threads.append(threading.Thread(target=gpu_worker, daemon=True))
@@ -455,6 +462,7 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
         th.start()
     for th in threads:
         th.join()
+    sys.setswitchinterval(prev_switch)
     torch.set_num_threads(prev_threads)
     if fail.exc is not None:
         raise RuntimeError("hybrid plan execution failed") from fail.exc
@@ -522,26 +530,58 @@ def measure_link_bandwidth(device, nbytes: int = 64 * 2**20, reps: int = 5) -> f
     return (nbytes / MB) / statistics.median(ts)
 
 
+def measure_link_latency(device, reps: int = 20) -> float:
+    """Fixed cost (ms) of one plan-boundary crossing as ``execute`` performs it:
+    a small pinned device->host copy on a copy stream and the host thread's
+    wait on its event (the reference's comm_time has only the byte term,
+    costmodel.py:133-139; profile_ops folds this latency into C so the
+    planner's crossing cost is the measured one)."""
+    src = torch.zeros(256, device=device)
+    dst = torch.empty(256).pin_memory()
+    st = torch.cuda.Stream(device)
+    ts = []
+    for _ in range(reps + 2):
+        ev = torch.cuda.Event()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(st):
+            dst.copy_(src, non_blocking=True)
+            ev.record(st)
+        ev.synchronize()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return statistics.median(ts[2:])
+
+
 def _host_cell_ms(host_rnn: HostRNN, ld: int, j: int, reps: int) -> float:
     """Median ms of one host cell of layer-direction ``ld`` while ``j`` cells
     run concurrently on ``j`` single-threaded workers (the reference's
-    "time when j cores are busy" column, costmodel.py:47-61)."""
+    "time when j cores are busy" column, costmodel.py:47-61).  Timed as the
+    hybrid executor's host worker runs a cell: the cell's ops plus the writes
+    of its outputs into the host activation and state mirrors."""
     spec = host_rnn.spec
     l = ld // spec.dirs
+    d = ld % spec.dirs
+    H = spec.hidden
     gen = torch.Generator().manual_seed(ld)
     xin = torch.rand((spec.batch, spec.layer_input(l)), generator=gen)
-    hp = torch.rand((spec.batch, spec.hidden), generator=gen)
+    hp = torch.rand((spec.batch, H), generator=gen)
     cp = hp.clone() if spec.cell == "lstm" else None
     times = [[] for _ in range(j)]
     barrier = threading.Barrier(j)
 
     def work(i):
         torch.set_num_threads(1)
+        act = torch.zeros((2, spec.batch, spec.dirs * H))
+        hs_ = torch.zeros((2, spec.batch, H))
+        cs_ = torch.zeros((2, spec.batch, H))
         host_rnn.cell(ld, xin, hp, cp)
         for _ in range(reps):
             barrier.wait()
             t0 = time.perf_counter()
-            host_rnn.cell(ld, xin, hp, cp)
+            h, c = host_rnn.cell(ld, xin, hp, cp)
+            act[1, :, d * H:(d + 1) * H] = h
+            hs_[1] = h
+            if c is not None:
+                cs_[1] = c
             times[i].append((time.perf_counter() - t0) * 1e3)
 
     prev = torch.get_num_threads()
@@ -557,14 +597,19 @@ def _host_cell_ms(host_rnn: HostRNN, ld: int, j: int, reps: int) -> float:
 def profile_ops(graph: Graph, model, k: int | None = None, reps: int = 5, b: float | None = None) -> CostModel:
     """Measured cost model of the RNN cell grid (drop-in for ``synth_profile``).
 
-    * ``W[:, 0]``: B200 ms per cell — each layer's fused forward time (K1 GEMM
-      + recurrent wavefront, CUDA events, median of ``reps``) divided by its
-      ``T * D`` cells, so an all-GPU plan's modelled latency equals the
-      measured forward.  Needs an RNNExecutor; with a
-      HostRNN the GPU column is +inf-free large (host column x 1e3) so no plan
-      selects the GPU.
+    * ``W[:, 0]``: B200 ms per cell from ``hs_rnn_profile_cells`` — each
+      cell's measured recurrence step (per-step %globaltimer stamps), scaled
+      so the cells sum to the measured forward (CUDA events), median of
+      ``reps``.  An all-GPU plan's modelled latency therefore equals the
+      measured forward, and the split between cells follows
+      the measured steps (e.g. the wavefront's pipeline fill).  Hybrid plans'
+      GPU segments run the same tensor-core kernels (``hs_rnn_run_cells``).
+      Needs an RNNExecutor; with a HostRNN the GPU column is the host column
+      x 1e3 so no plan selects the GPU.
     * ``W[:, j]``, j = 1..k: host ms per cell with ``j`` cells running at once.
-    * ``C[m, i]``: MB moved on each edge (h, plus c on LSTM state edges).
+    * ``C[m, i]``: MB moved on each edge (h, plus c on LSTM state edges),
+      plus the measured per-crossing latency x ``b`` (``measure_link_latency``),
+      so ``comm_time = C / b`` (costmodel.py:133-139) is bytes / b + latency.
     * ``Mem[i]``: (input, output, ephemeral gates, weights) MB, on MEM_GRID.
     * ``b``: measured pinned H2D MB/ms (or the given value).
     """
@@ -593,23 +638,20 @@ def profile_ops(graph: Graph, model, k: int | None = None, reps: int = 5, b: flo
         x = torch.rand((T, B, spec.I), generator=torch.Generator().manual_seed(1)).to(dev)
         outs = model.alloc_outputs()
         model.forward(x, out=outs)
-        per_layer = []
-        for _ in range(reps):
-            *_, lm = model.forward(x, out=outs, layer_ms=True)
-            per_layer.append([g + r for g, r in lm])
-        layer_ms = [statistics.median(p[l] for p in per_layer) for l in range(L)]
-        for v in range(n):
-            W[v, 0] = layer_ms[(v // T) // D] / (T * D)
+        runs = [model.profile_cells(x, out=outs)[0] for _ in range(reps)]
+        W[:, 0] = np.median(np.asarray(runs, dtype=np.float64), axis=0)
         if b is None:
             b = measure_link_bandwidth(dev)
+        lat_ms = measure_link_latency(dev)
     else:
         W[:, 0] = W[:, 1] * 1e3
         if b is None:
             b = 16.0
+        lat_ms = 0.0
     C = np.zeros((n, n))
     for s, d in graph.edge_set:
         same_chain = (s // T) == (d // T)
-        C[s, d] = (B * H * 4 * (2 if (lstm and same_chain) else 1)) / MB
+        C[s, d] = (B * H * 4 * (2 if (lstm and same_chain) else 1)) / MB + lat_ms * b
     Mem = np.empty((n, 4))
     for v in range(n):
         l = (v // T) // D

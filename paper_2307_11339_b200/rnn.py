@@ -49,6 +49,7 @@ ABI_SYMBOLS = (
     "hs_rnn_packed_size",
     "hs_rnn_pack_weights",
     "hs_rnn_forward_packed",
+    "hs_rnn_profile_cells",
     "hs_rnn_forward",
     "hs_rnn_forward_host",
     "hs_rnn_run_cells",
@@ -176,6 +177,8 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_packed_size.argtypes = [pd, ctypes.POINTER(sz)]
     lib.hs_rnn_pack_weights.argtypes = [pd, pvp, pvp, pvp, pvp, vp, sz, vp]
     lib.hs_rnn_forward_packed.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, ctypes.POINTER(ctypes.c_float)]
+    fp = ctypes.POINTER(ctypes.c_float)
+    lib.hs_rnn_profile_cells.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, fp, fp]
     lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
@@ -389,6 +392,37 @@ class RNNExecutor:
         if layer_ms:
             return y, hn, cn, [[times[2 * l], times[2 * l + 1]] for l in range(s.layers)]
         return y, hn, cn
+
+    def profile_cells(self, x: torch.Tensor, h0=None, c0=None, out=None):
+        """Per-cell GPU cost (ms) of the whole-DAG forward, ``hs_rnn_profile_cells``:
+        ``[layers*dirs*T]`` indexed like the cell grid's nodes, summing to the
+        measured forward.  Returns ``(cell_ms, forward_ms)``."""
+        self._require_resident()
+        s = self.spec
+        if x.device != self.device or x.dtype != torch.float32 or not x.is_contiguous():
+            raise ValueError("x must be a contiguous float32 tensor on the executor's device")
+        if tuple(x.shape) != (s.seq, s.batch, s.I):
+            raise ValueError(f"x has shape {tuple(x.shape)}, expected {(s.seq, s.batch, s.I)}")
+        state = (s.layers * s.dirs, s.batch, s.hidden)
+        self._check_dev("h0", h0, state)
+        self._check_dev("c0", c0 if s.cell == "lstm" else None, state)
+        y, hn, cn = out if out is not None else self.alloc_outputs()
+        n = s.layers * s.dirs * s.seq
+        cells = (ctypes.c_float * n)()
+        fwd = ctypes.c_float()
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            _check(
+                self.lib,
+                "hs_rnn_profile_cells",
+                self.lib.hs_rnn_profile_cells(
+                    ctypes.byref(self.desc), self.packed.data_ptr(), x.data_ptr(), ptr(h0), ptr(c0),
+                    y.data_ptr(), hn.data_ptr(), ptr(cn), self.workspace.data_ptr(), self.workspace.numel(),
+                    stream.cuda_stream, cells, ctypes.byref(fwd),
+                ),
+            )
+        return [float(v) for v in cells], float(fwd.value)
 
     def alloc_host_outputs(self):
         """Pinned host output buffers (y, h_n, c_n) for :meth:`forward_host`."""

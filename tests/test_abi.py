@@ -104,3 +104,19 @@ def test_plan_query_without_gpu():
     assert c3[0] == 2 and c3[2] == 0
     assert c4[0] == 2 and c4[2] > 0                          # W_hh 64 MiB/layer: streamed ring
     assert c5[0] == 2 and c5[3] > 1                          # bf16, batch sliced on one GPU
+
+
+def test_integration_stub_descriptor_matches_the_header():
+    """The ctypes stub INTEGRATION.md shows a maintainer declares the same
+    descriptor layout as include/hs_rnn.h (and the package's own binding)."""
+    doc = (HEADER.parents[1] / "INTEGRATION.md").read_text()
+    block = re.search(r"```python\n(import ctypes\n\nclass hs_rnn_desc.*?)\nlib = ", doc, re.S).group(1)
+    ns = {}
+    exec(block, ns)
+    stub = ns["hs_rnn_desc"]
+    assert ctypes.sizeof(stub) == ctypes.sizeof(rnn._Desc)
+    hdr = HEADER.read_text()
+    body = re.search(r"typedef struct hs_rnn_desc \{(.*?)\} hs_rnn_desc;", hdr, re.S).group(1)
+    named = re.findall(r"int32_t (\w+);", body)
+    assert [f[0] for f in stub._fields_ if f[0] != "reserved"] == named
+    assert [f[0] for f in rnn._Desc._fields_ if f[0] != "reserved"] == named

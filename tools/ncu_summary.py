@@ -2,6 +2,8 @@
 
   python tools/ncu_summary.py <report.ncu-rep> [...]      -> markdown table on stdout
   python tools/ncu_summary.py --launches <launches.csv>   -> per-kernel share table
+  python tools/ncu_summary.py --raw <raw.csv> [...]        -> the same table from `ncu -i X --page raw --csv`
+                                                              exported on the GPU box
 """
 import collections
 import csv
@@ -27,12 +29,22 @@ KEYS = [
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
+    "lts__t_sectors_srcunit_tex_lookup_hit.sum",
+    "lts__t_sectors_srcunit_tex_lookup_miss.sum",
+    "lts__t_sectors_srcunit_tex_evict_last_lookup_hit.sum",
+    "lts__t_sectors_srcunit_tex_evict_last_lookup_miss.sum",
+    "lts__t_sectors_srcunit_tex.sum.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum.per_second",
 ]
 
 
-def report(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def report(path, raw_text=None):
+    out = raw_text if raw_text is not None else subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                                                               capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    rows = rows[start:]
     hdr, units = rows[0], rows[1]
     print(f"### {path}\n")
     for r in rows[2:]:
@@ -67,6 +79,9 @@ def launches(path):
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--raw":
+        for p in sys.argv[2:]:
+            report(p, open(p).read())
     else:
         for p in sys.argv[1:]:
             report(p)

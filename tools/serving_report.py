@@ -80,6 +80,7 @@ def main():
                "footprint_mb": e.gpu_footprint_mb, "weights_mb": e.weights_mb, "gpu_request_ms": e.exec_latency_ms,
                "slo_ms": e.slo_ms}
         if not args.no_patterns:
+            ex.load()  # the probe's measurements leave models offloaded
             g = hs.gen_lstm_grid(spec.layers, spec.seq)
             x = hs.make_input(spec)
             cm = hs.profile_ops(g, ex, k=4, reps=3)
