@@ -282,7 +282,7 @@ def reference_planner():
         return None
 
 
-def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_mhz=None, sms=148):
+def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_mhz=None, sms=148, l2_peak=None):
     """Roofline of the dominant kernel, the recurrence: t_roof = max(FLOPs /
     tensor peak, bytes / HBM bandwidth), so frac = max of the two fractions and
     `bound` names the larger.  FLOPs: the algorithmic recurrent FLOPs.  Bytes:
@@ -298,8 +298,13 @@ def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_
     G, H, B, T = spec.G, spec.hidden, spec.batch, spec.seq
     wbytes = (2.0 if spec.dtype == "bf16" else 4.0) * G * H * H
     slices = max(1, plan.get("batch_slices", 1))
-    per_step = (wbytes * slices if plan.get("w_ring") else 0.0) + 4.0 * B * G * H + 4.0 * B * H
-    nbytes = T * spec.layers * spec.dirs * per_step
+    LD = spec.layers * spec.dirs
+    # HBM: xproj read + y write per step, and W_hh once per launch when it is
+    # streamed (ncu, profiles/r02_summary.md: the W ring's per-step re-reads
+    # hit L2 — c4 99.8% of 34 GB of evict_last sectors — so they are L2, not
+    # HBM, traffic; see the "l2" entry below)
+    streamed = bool(plan.get("w_ring"))
+    nbytes = T * LD * (4.0 * B * G * H + 4.0 * B * H) + (wbytes * slices * LD if streamed else 0.0)
     gbs = nbytes / sec / 1e9
     f_hbm = gbs / peaks["hbm_gbs"]
     tensor = dict(achieved=tf, peak=peaks["bf16_tflops"], unit="TFLOP/s", frac=f_tensor, algorithmic_flops=rec_f,
@@ -310,6 +315,12 @@ def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_
         out = dict(common, bound="hbm", **hbm, other={"bound": "tensor", **tensor})
     else:
         out = dict(common, bound="tensor", **tensor, other={"bound": "hbm", **hbm})
+    if streamed and l2_peak:
+        l2b = wbytes * slices * T * LD
+        out["l2"] = {"achieved": l2b / sec / 1e9, "peak": l2_peak["gbs"], "unit": "GB/s",
+                     "frac": l2b / sec / 1e9 / l2_peak["gbs"], "bytes": l2b,
+                     "what": "W_hh ring re-reads, one per step per batch slice (served from L2)",
+                     "peak_source": l2_peak["source"]}
     if spec.dtype == "f32" and sm_mhz:
         # SURVEY §8d's K2/K3 roofline for fp32 mode: t_roof = max(F_rec / P_FFMA,
         # streamed W_hh bytes / HBM), P_FFMA = SMs x 128 FP32 lanes x 2 x the SM
@@ -551,6 +562,9 @@ def main(argv=None):
     if tfile.exists():
         tdoc = json.loads(tfile.read_text())
         traffic = tdoc.get(f"{args.config}:{ex.algo}:recurrent")
+        l2_peak = tdoc.get("_l2_peak")
+    else:
+        l2_peak = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": p90,
@@ -562,7 +576,7 @@ def main(argv=None):
                    "e2e_l2": "no flush; per-request working set (2 x 128 MiB xproj + 32 MiB x + 32 MiB y) exceeds the 126 MB L2"},
         "roofline": roofline_entry(spec, plan, ex.algo, rec_f, rec_ms, gemm_ms, peaks, traffic,
                                    sm_mhz=clocks.summary().get("sm_mhz"),
-                                   sms=torch.cuda.get_device_properties(dev).multi_processor_count),
+                                   sms=torch.cuda.get_device_properties(dev).multi_processor_count, l2_peak=l2_peak),
         "plan": plan,
         "e2e": {"value": B_total * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,

@@ -290,6 +290,28 @@ def _wait(evt: threading.Event, fail: _Failure):
             raise RuntimeError("hybrid execution aborted") from fail.exc
 
 
+_POOL = None
+_POOL_LOCK = threading.Lock()
+
+
+def _worker_pool(n: int):
+    """Process-wide pool of plan workers (one thread per host core of a plan,
+    plus the GPU queue's).  Threads persist across ``execute`` calls: a fresh
+    thread per call cost ~0.3 ms to start and ~0.4 ms more for its first
+    cell (per-thread runtime setup), which the cost model has no term for."""
+    global _POOL
+    from concurrent.futures import ThreadPoolExecutor
+
+    with _POOL_LOCK:
+        if _POOL is None or _POOL._max_workers < n:
+            old = _POOL
+            _POOL = ThreadPoolExecutor(max_workers=max(n, 4), thread_name_prefix="hs-plan",
+                                       initializer=torch.set_num_threads, initargs=(1,))
+            if old is not None:
+                old.shutdown(wait=False)
+        return _POOL
+
+
 def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResult:
     spec = model.spec
     host_rnn = _host_model(model)
@@ -426,7 +448,6 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
     # ----------------------------------------------------------- host side
     def host_worker(core, queue):
         try:
-            torch.set_num_threads(1)
             for v in queue:
                 l, d, t, s = cells[v]
                 ld = l * D + d
@@ -449,21 +470,18 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
         except BaseException as exc:
             fail.set(exc)
 
-    prev_threads = torch.get_num_threads()
     # cells hand off between worker threads at every crossing: a short GIL
     # switch interval (default 5 ms) keeps a woken waiter from queueing behind
     # a running worker for a whole interval
     prev_switch = sys.getswitchinterval()
     sys.setswitchinterval(5e-5)
-    threads = [threading.Thread(target=host_worker, args=(c, q), daemon=True) for c, q in sorted(sched.host.items())]
+    tasks = [(host_worker, (c, q)) for c, q in sorted(sched.host.items())]
     if uses_gpu:
-        threads.append(threading.Thread(target=gpu_worker, daemon=True))
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join()
+        tasks.append((gpu_worker, ()))
+    pool = _worker_pool(len(tasks))
+    for fut in [pool.submit(fn, *args) for fn, args in tasks]:
+        fut.result()
     sys.setswitchinterval(prev_switch)
-    torch.set_num_threads(prev_threads)
     if fail.exc is not None:
         raise RuntimeError("hybrid plan execution failed") from fail.exc
 
