@@ -170,6 +170,52 @@ int hs_rnn_forward(const hs_rnn_desc* desc, const void* x,
                    const void* h0, const void* c0, void* y, void* hn, void* cn,
                    void* workspace, size_t ws_bytes, void* stream);
 
+/* Layer-pipeline stage link (the modelled link of
+ * costmodel.py:133-139 / engine.py:317-339 made real).  A stage owns a range
+ * of layers; its input arrives from the previous stage, its output goes to
+ * the next, as bf16 hi/lo activation planes [2][T*B][I] (the layout the next
+ * layer's input-projection GEMM reads) copied GPU-to-GPU by the copy engine
+ * (NVLink P2P) in time chunks while the producing recurrence still runs.
+ * All synchronisation is stream-ordered (cuStreamWaitValue32 /
+ * cuStreamWriteValue32 on 32-bit words); no kernel spins on another GPU.
+ * Counters are monotonic across requests, so they are never reset:
+ *   x_avail   (consumer-owned) = x_base + timesteps of the current request
+ *             present in x_planes; written by the producer after each chunk.
+ *   consumed  (producer-owned) = set by the consumer to consumed_value once
+ *             it has read its x_planes slot (its input GEMM is done with it).
+ * Pointers to the peer's words / planes are mapped into this process by the
+ * caller (CUDA IPC; paper_2307_11339_b200/parallel.py does it with
+ * torch.multiprocessing's CUDA tensor sharing). */
+typedef struct hs_stage_link {
+  /* input side: NULL x_planes = the stage reads `x` (fp32) like a forward */
+  const void* x_planes;           /* [2][T*B][I] bf16 hi/lo planes of this request's input */
+  const uint32_t* x_avail;        /* local word the previous stage advances */
+  uint32_t x_base;                /* value of *x_avail before this request's first chunk */
+  uint32_t consumed_value;        /* written to *consumed_peer after the last read of x_planes */
+  uint32_t* consumed_peer;        /* the previous stage's `consumed` word (peer memory) or NULL */
+  /* output side: NULL y_peer_planes = no next stage (y is the model output) */
+  void* y_peer_planes;            /* the next stage's x_planes slot for this request (peer memory) */
+  uint32_t* y_peer_avail;         /* the next stage's x_avail word (peer memory) */
+  uint32_t y_base;                /* *y_peer_avail before this request's first chunk */
+  uint32_t consumed_wait;         /* wait until *consumed >= this before the first copy into the slot */
+  const uint32_t* consumed;       /* local word the next stage advances (NULL = slot always free) */
+  int32_t chunks;                 /* hand-off chunks per request (0 = 16) */
+  int32_t reserved[5];
+} hs_stage_link;
+
+/* One pipeline stage's forward (tensor-core path, unidirectional): as
+ * hs_rnn_forward_packed over this stage's layers, with the input taken from
+ * link->x_planes chunk by chunk as x_avail advances (the first layer's input
+ * projection runs per arrived chunk), and the last layer's output shipped to
+ * the next stage chunk by chunk as its recurrence publishes steps.  `y`
+ * ([T, B, H] fp32) is written on every stage.  All work, copies and peer
+ * signals included, is ordered on `stream`.  Replaces: the chunked
+ * NCCL isend/irecv hand-off of parallel.LayerPipeline (round 1). */
+int hs_rnn_forward_stage(const hs_rnn_desc* desc, const void* packed,
+                         const void* x, const void* h0, const void* c0,
+                         void* y, void* hn, void* cn, const hs_stage_link* link,
+                         void* workspace, size_t ws_bytes, void* stream);
+
 /* One GPU segment of a plan: timesteps t0..t1-1 (in the direction's own
  * processing order) of layer-direction `ld`.  On the tensor-core path the
  * segment runs the fused forward's kernels (split + K1 GEMM over the

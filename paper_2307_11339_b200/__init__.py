@@ -72,7 +72,7 @@ from .planner import (
 )
 from .rnn import CONFIGS, RNNExecutor, RNNSpec, init_weights, load_library, make_input
 from .executor import ExecResult, HostRNN, build_schedule, execute, measure_link_bandwidth, profile_ops
-from .parallel import HostStage, LayerPipeline, RequestShard, shard_range, stage_layers
+from .parallel import HostStage, LayerPipeline, PeerPipeline, RequestShard, shard_range, stage_layers
 from .serve import InferenceRequest, InferenceResponse, RNNServer, register_model, run
 
 __all__ = [
@@ -96,5 +96,5 @@ __all__ = [
     "HostRNN", "ExecResult", "build_schedule", "execute", "profile_ops", "measure_link_bandwidth",
     "InferenceRequest", "InferenceResponse", "RNNServer", "register_model", "run",
     # multi-GPU
-    "RequestShard", "LayerPipeline", "HostStage", "shard_range", "stage_layers",
+    "RequestShard", "LayerPipeline", "PeerPipeline", "HostStage", "shard_range", "stage_layers",
 ]

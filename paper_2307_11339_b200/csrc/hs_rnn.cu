@@ -384,6 +384,7 @@ struct Overlap {
   float* y_host = nullptr;
   cudaStream_t cs_in = nullptr;   // x uploads (H2D)
   cudaStream_t cs_out = nullptr;  // y downloads (D2H); separate so PCIe runs both directions at once
+  const hs_stage_link* link = nullptr;  // layer-pipeline stage (hs_rnn_forward_stage); cs_out ships y
 };
 
 // Per x staging buffer: an event recorded once the forward has consumed it
@@ -428,6 +429,21 @@ WaitValue32Fn wait_value_fn() {
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<WaitValue32Fn>(p);
     if (getenv("HS_DEBUG")) fprintf(stderr, "[hsrnn] cuStreamWaitValue32 %s\n", fn ? "available" : "unavailable");
+  }
+  return fn;
+}
+
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value_fn() {
+  static WriteValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
   }
   return fn;
 }
@@ -837,6 +853,13 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   static const char* xreq_env = getenv("HS_REQ_OVERLAP");
   const bool xreq_ok = overlap && m.L % 2 == 0 && gemm_bn(m.G * m.H) == 256 && !(xreq_env && atoi(xreq_env) == 0);
   const bool chunked_in = ov && ov->x_host;
+  // layer-pipeline stage: input planes arrive from the previous stage in
+  // chunks (peer_in), the last layer's output planes go to the next (peer_out)
+  const hs_stage_link* lk = ov ? ov->link : nullptr;
+  const bool peer_in = lk && lk->x_planes;
+  const bool peer_out = lk && lk->y_peer_planes;
+  const int link_chunks = lk ? (lk->chunks > 0 ? (lk->chunks < m.T ? lk->chunks : m.T) : (m.T < 16 ? m.T : 16)) : 0;
+  if (lk) wp = WavePlan{};  // stages run their layers one launch after another
   if (chunked_in && xreq_ok && (m.T < m.upload_chunks ? m.T : m.upload_chunks) == 1) {
     cudaEvent_t x_free;
     bool seen;
@@ -909,6 +932,30 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       }
     }
     HS_CUDA(cudaEventRecord(x_free, s));  // x consumed: the next upload into it may start
+  } else if (peer_in) {
+    // the previous stage's output planes land chunk by chunk; each chunk's
+    // input projection runs once its rows are present (x_avail, advanced by
+    // the producer's copy stream after each chunk)
+    WaitValue32Fn wait = wait_value_fn();
+    WriteValue32Fn write = write_value_fn();
+    if (!wait || !write) return fail(HS_ERR_UNSUPPORTED, "pipeline stages need CUDA stream memory operations");
+    const __nv_bfloat16* xin = static_cast<const __nv_bfloat16*>(lk->x_planes);
+    for (int k = 0; k < link_chunks; ++k) {
+      int t0, t1;
+      chunk_bounds(m.T, link_chunks, k, &t0, &t1);
+      const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
+      CUresult r = wait(s, reinterpret_cast<CUdeviceptr>(lk->x_avail), lk->x_base + (cuuint32_t)t1, 0 /*GEQ*/);
+      if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, pl.ld[0].tc);
+      float* xp = at<float>(ws, wl.xproj);
+      rc = gemm_planes(xin + r0 * m.I, wih, at<float>(packed, pl.ld[0].bias_x), xp + r0 * m.G * m.H, (int)nr,
+                       m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err, TB * m.I);
+      if (rc) return rc;
+    }
+    if (lk->consumed_peer) {  // the slot may be refilled by the previous stage
+      CUresult r = write(s, reinterpret_cast<CUdeviceptr>(lk->consumed_peer), lk->consumed_value, 0);
+      if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    }
   } else {
     rc = split_planes(x, xpl, TB, m.I, s, g_err);
     if (rc) return rc;
@@ -930,7 +977,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   // two running concurrently: off where launches are serialised (profilers,
   // sanitizers, CUDA_LAUNCH_BLOCKING: kernels_run_concurrently) and, per layer
   // below, unless >= 16 SMs stay free beside the recurrence.
-  const bool xstream = overlap && !chunked_in && gemm_bn(m.G * m.H) == 256 &&
+  const bool xstream = overlap && !chunked_in && !lk && gemm_bn(m.G * m.H) == 256 &&
                        (xs_env ? atoi(xs_env) == 1 : k1_flop >= 100e9) && kernels_run_concurrently();
   char xp_key[160];
   {
@@ -945,10 +992,11 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     float* xpl_l = xpb[overlap ? (l & 1) : 0];
     // streamed only where the recurrence's in-place ypl writes (row t, after its
     // M-tile's K1 tiles are stored) line up with the K1 input rows: Il == D*H
-    const bool xs_layer = xstream && !(chunked_in && l == 0) && Il == m.D * m.H;
+    const bool pre_k1 = (chunked_in || peer_in) && l == 0;  // layer 0's K1 ran in the prologue
+    const bool xs_layer = xstream && !pre_k1 && Il == m.D * m.H;
     // this layer's K1 as one launch on s before the recurrence: not streamed and
     // not already computed (host-upload chunks for layer 0, next-layer overlap)
-    const bool k1_now = !(chunked_in && l == 0) && !xs_layer && !(overlap && !xstream && l > 0);
+    const bool k1_now = !pre_k1 && !xs_layer && !(overlap && !xstream && l > 0);
     if (overlap && l > 0 && (rc = join(gs, s))) return rc;  // layer l's K1 chunks done
     TcRecurArgs a{};
     a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = m.D; a.Bst = m.B;
@@ -973,7 +1021,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     }
     const bool last = l == m.L - 1;
     a.y = last ? y : nullptr;
-    a.ypl = last ? nullptr : xpl;
+    a.ypl = last && !peer_out ? nullptr : xpl;  // a stage's last layer writes the next stage's input planes
     a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
     a.stamps = g_stamps ? g_stamps + (size_t)l * m.D * (m.T + 1) : nullptr;
@@ -1013,6 +1061,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     auto tnow = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     const double tz = dbg_host ? tnow() : 0.0;
     const bool drain = last && ov && ov->y_host;
+    const bool ship = last && peer_out;  // copy the output planes to the next stage as steps complete
     const bool feed_next = overlap && !last && !xstream;
     // two batch-half groups per CTA (tc_recur2.cuh) when the batch is large
     // enough for both chains to carry work: c2 (B=64) 6.85 -> 6.58 us/step;
@@ -1080,10 +1129,10 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         if (xevs) HS_CUDA(cudaEventRecord(xevs[0], s));
       }
     }
-    if (drain || feed_next) {
+    if (drain || feed_next || ship) {
       a.progress = reinterpret_cast<unsigned int*>(tcws + tw.progress);  // zeroed with the layer's regions above
       // counters zeroed before the copy / K1 stream polls them
-      if (drain && (rc = join(s, ov->cs_out))) return rc;
+      if ((drain || ship) && (rc = join(s, ov->cs_out))) return rc;
       if ((feed_next || (drain && xreq_ok)) && (rc = join(s, gs))) return rc;
     }
     static const bool dbg = getenv("HS_DEBUG_HOSTIO") != nullptr;
@@ -1193,6 +1242,32 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
                            m.G * m.H, In, NPL == 2 ? 3 : 1, gs, g_err, TB * In, /*persistent=*/false);
           if (rc) return rc;
         }
+      }
+    }
+    if (ship) {
+      // output planes of chunk [t0, t1) are final once every recurrence CTA
+      // has published step t1-1: copy them into the next stage's slot (peer
+      // memory, NVLink) and advance its x_avail, all on the copy stream
+      const unsigned int ncta = (unsigned int)(a.D * a.RB * a.S) * (two ? kNG : 1);
+      WaitValue32Fn wait = wait_value_fn();
+      WriteValue32Fn write = write_value_fn();
+      if (!wait || !write || nsl != 1) return fail(HS_ERR_UNSUPPORTED, "pipeline hand-off needs stream memory operations and an unsliced batch");
+      if (lk->consumed) {  // the next stage has read this slot's previous request
+        CUresult r = wait(ov->cs_out, reinterpret_cast<CUdeviceptr>(lk->consumed), lk->consumed_wait, 0 /*GEQ*/);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      }
+      const size_t row = (size_t)m.B * m.H, plane = TB * m.H;
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(lk->y_peer_planes);
+      for (int k = 0; k < link_chunks; ++k) {
+        int t0, t1;
+        chunk_bounds(m.T, link_chunks, k, &t0, &t1);
+        CUresult r = wait(ov->cs_out, reinterpret_cast<CUdeviceptr>(a.progress + t1 - 1), ncta, 0 /*GEQ*/);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        for (int p = 0; p < 2; ++p)
+          HS_CUDA(cudaMemcpyAsync(dst + p * plane + (size_t)t0 * row, xpl + p * plane + (size_t)t0 * row,
+                                  (size_t)(t1 - t0) * row * sizeof(__nv_bfloat16), cudaMemcpyDefault, ov->cs_out));
+        r = write(ov->cs_out, reinterpret_cast<CUdeviceptr>(lk->y_peer_avail), lk->y_base + (cuuint32_t)t1, 0);
+        if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
       }
     }
     if (drain) {
@@ -1610,6 +1685,41 @@ int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed, const void
     }
   }
   for (size_t i = 0; i < per.size(); ++i) cell_ms[i] = (float)(per[i] * (double)fwd / sum);
+  return HS_OK;
+}
+
+int hs_rnn_forward_stage(const hs_rnn_desc* desc, const void* packed, const void* x, const void* h0, const void* c0,
+                         void* y, void* hn, void* cn, const hs_stage_link* link, void* workspace, size_t ws_bytes,
+                         void* stream) {
+  hs::g_launch_count = 0;
+  Dims m;
+  int rc = check_desc(desc, &m);
+  if (rc) return rc;
+  if (!link) return fail(HS_ERR_INVALID, "link must be non-NULL (use hs_rnn_forward_packed for a whole model)");
+  if (!packed || (!x && !link->x_planes) || !y || !hn || !workspace)
+    return fail(HS_ERR_INVALID, "packed, x (or link->x_planes), y, hn and workspace must be non-NULL");
+  if (m.G == 4 && !cn) return fail(HS_ERR_INVALID, "LSTM needs a c_n output");
+  if (m.D != 1) return fail(HS_ERR_UNSUPPORTED, "bidirectional layers cannot be pipelined over time");
+  if (link->x_planes && !link->x_avail) return fail(HS_ERR_INVALID, "link->x_planes needs link->x_avail");
+  if (link->y_peer_planes && !link->y_peer_avail) return fail(HS_ERR_INVALID, "link->y_peer_planes needs link->y_peer_avail");
+  DeviceInfo di;
+  if ((rc = device_info(&di))) return rc;
+  int algo;
+  if ((rc = resolve_algo(m, &algo))) return rc;
+  if (algo != HS_ALGO_TC) return fail(HS_ERR_UNSUPPORTED, "pipeline stages run on the tensor-core path only");
+  PackLayout pl;
+  if ((rc = pack_layout(m, &pl))) return rc;
+  WsLayout wl = ws_layout(m);
+  if (ws_bytes < wl.total) return fail(HS_ERR_WORKSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, wl.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Overlap ov;
+  ov.link = link;
+  if ((rc = copy_stream(1, &ov.cs_out))) return rc;
+  rc = forward_impl(m, algo, di, pl, packed, static_cast<const float*>(x), static_cast<const float*>(h0),
+                    static_cast<const float*>(c0), static_cast<float*>(y), static_cast<float*>(hn),
+                    static_cast<float*>(cn), workspace, wl, s, nullptr, &ov);
+  if (rc) return rc;
+  if (link->y_peer_planes && (rc = join(ov.cs_out, s))) return rc;  // the hand-off copies end inside the call's stream order
   return HS_OK;
 }
 

@@ -19,6 +19,16 @@ The path shards two ways, and neither needs a collective:
   layer l+1 at t needs layer l's backward output at t, which is produced
   last. Those stacks use request sharding.
 
+  With ``handoff="peer"`` (:class:`PeerPipeline`) each stage instead runs
+  the whole sequence in ONE stage forward (``hs_rnn_forward_stage``): its last
+  layer's output planes are copied GPU-to-GPU by the copy engine into the
+  next stage's input slot, chunk by chunk as the recurrence publishes steps,
+  and the next stage's input projection consumes each chunk as it lands.
+  Synchronisation is stream-ordered on monotonic 32-bit counters in GPU
+  memory (cuStreamWaitValue32 / cuStreamWriteValue32), shared between the
+  processes by CUDA IPC; no kernel spins on another GPU and there is no NCCL
+  call on the data path. No relaunch per chunk, no W_hh reload.
+
 The reference has no multi-device execution: its "devices" are virtual
 processors inside one process (costmodel.py:3-11, engine.py:37; SPEC.md:451
 lists multi-GPU clusters as a non-goal). Plans carry no GPU index, so these
@@ -34,7 +44,8 @@ import torch.distributed as dist
 
 from .rnn import RNNSpec
 
-__all__ = ["shard_range", "stage_layers", "RequestShard", "LayerPipeline", "HostStage"]
+__all__ = ["shard_range", "stage_layers", "RequestShard", "LayerPipeline", "HostStage", "PeerPipeline",
+           "stage_link_values"]
 
 
 def shard_range(batch: int, world: int, rank: int) -> tuple[int, int]:
@@ -249,3 +260,123 @@ class LayerPipeline:
             if w is not None:
                 w.wait()
         return results
+
+
+# ------------------------------------------------------- peer (K4) hand-off
+
+def stage_link_values(r: int, T: int, rank: int, world: int) -> dict:
+    """Counter values of global request ``r`` on stage ``rank`` (monotonic, so
+    they are never reset; include/hs_rnn.h ``hs_stage_link``):
+
+    * input: the slot is ``r % 2``; x_avail reaches ``x_base + T`` when the
+      whole request has landed; after reading it the stage sets the previous
+      stage's ``consumed`` word to ``r + 1``;
+    * output: before the first copy into the next stage's slot ``r % 2`` the
+      stage waits for ``consumed >= r - 1`` (request ``r - 2``, the slot's
+      previous occupant, has been read).
+    """
+    v = {"slot": r % 2}
+    if rank > 0:
+        v.update(x_base=r * T, consumed_value=r + 1)
+    if rank < world - 1:
+        v.update(y_base=r * T, consumed_wait=max(0, r - 1))
+    return v
+
+
+def _share(t: torch.Tensor):
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    return reduce_tensor(t)
+
+
+def _open(shared):
+    fn, args = shared
+    return fn(*args)
+
+
+class PeerPipeline:
+    """Stage ``rank`` of a layer pipeline with the stream-ordered peer hand-off.
+
+    ``executor`` is this stage's :class:`~.rnn.RNNExecutor` (its spec has the
+    stage's layers, the full sequence and input width ``I`` on stage 0, ``H``
+    elsewhere).  Buffers shared with the neighbours over CUDA IPC:
+
+    * consumer side (rank > 0): two input slots of bf16 hi/lo planes
+      ``[2][2][T*B][I]`` and the ``x_avail`` word;
+    * producer side (rank < world-1): the ``consumed`` word.
+
+    ``group`` is the process group used once, at construction, to exchange
+    the IPC handles (any backend; gloo works for same-host ranks).
+    """
+
+    def __init__(self, executor, rank: int, world: int, chunk: int = 32, group=None):
+        from .rnn import StageLink
+
+        self.ex, self.rank, self.world = executor, rank, world
+        s = executor.spec
+        if s.dirs != 1:
+            raise ValueError("bidirectional stacks cannot be layer-pipelined over time; use request sharding")
+        self.T, self.B = s.seq, s.batch
+        self.chunks = max(1, -(-s.seq // max(1, chunk)))
+        dev = executor.device
+        self._StageLink = StageLink
+        self.slots = self.x_avail = self.consumed = None
+        if rank > 0:
+            self.slots = torch.zeros((2, 2, s.seq * s.batch, s.I), dtype=torch.bfloat16, device=dev)
+            self.x_avail = torch.zeros(1, dtype=torch.int32, device=dev)
+        if rank < world - 1:
+            self.consumed = torch.zeros(1, dtype=torch.int32, device=dev)
+        mine = {"slots": _share(self.slots) if self.slots is not None else None,
+                "x_avail": _share(self.x_avail) if self.x_avail is not None else None,
+                "consumed": _share(self.consumed) if self.consumed is not None else None}
+        torch.cuda.synchronize(dev)
+        allv = [None] * world
+        dist.all_gather_object(allv, mine, group=group)
+        self.next_slots = self.next_avail = self.prev_consumed = None
+        if rank < world - 1:
+            nxt = allv[rank + 1]
+            self.next_slots = _open(nxt["slots"])
+            self.next_avail = _open(nxt["x_avail"])
+        if rank > 0:
+            self.prev_consumed = _open(allv[rank - 1]["consumed"])
+        self._keep = allv
+        self.seq = 0  # global request counter (the monotonic counters' base)
+
+    def link(self, r: int):
+        v = stage_link_values(r, self.T, self.rank, self.world)
+        lk = self._StageLink()
+        lk.chunks = self.chunks
+        if self.rank > 0:
+            lk.x_planes = self.slots[v["slot"]].data_ptr()
+            lk.x_avail = self.x_avail.data_ptr()
+            lk.x_base = v["x_base"]
+            lk.consumed_peer = self.prev_consumed.data_ptr()
+            lk.consumed_value = v["consumed_value"]
+        if self.rank < self.world - 1:
+            lk.y_peer_planes = self.next_slots[v["slot"]].data_ptr()
+            lk.y_peer_avail = self.next_avail.data_ptr()
+            lk.y_base = v["y_base"]
+            lk.consumed = self.consumed.data_ptr()
+            lk.consumed_wait = v["consumed_wait"]
+        return lk
+
+    def run_many(self, xs, h0s=None, c0s=None) -> list[PipelineResult]:
+        """A stream of requests.  Stage 0 needs ``xs`` (device or host
+        ``[T, B, I]``); other stages pass a list of ``None`` of the same
+        length.  Returns ``y`` on the last stage and this stage's final
+        states everywhere (copies; all work ordered on the current stream)."""
+        ex = self.ex
+        n = len(xs)
+        h0s = h0s or [None] * n
+        c0s = c0s or [None] * n
+        outs = []
+        for i in range(n):
+            r = self.seq + i
+            x = xs[i].to(ex.device, torch.float32).contiguous() if self.rank == 0 else None
+            y, hn, cn = ex.forward_stage(self.link(r), x=x, h0=h0s[i], c0=c0s[i])
+            outs.append(PipelineResult(y if self.rank == self.world - 1 else None, hn, cn))
+        self.seq += n
+        return outs
+
+    def run(self, x=None, h0=None, c0=None) -> PipelineResult:
+        return self.run_many([x], [h0], [c0])[0]

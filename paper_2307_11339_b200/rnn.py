@@ -52,6 +52,7 @@ ABI_SYMBOLS = (
     "hs_rnn_profile_cells",
     "hs_rnn_forward",
     "hs_rnn_forward_host",
+    "hs_rnn_forward_stage",
     "hs_rnn_run_cells",
 )
 
@@ -139,6 +140,26 @@ class _Desc(ctypes.Structure):
     ]
 
 
+class StageLink(ctypes.Structure):
+    """``hs_stage_link`` (include/hs_rnn.h): a layer-pipeline stage's input
+    and output hand-off (device pointers, monotonic 32-bit counters)."""
+
+    _fields_ = [
+        ("x_planes", ctypes.c_void_p),
+        ("x_avail", ctypes.c_void_p),
+        ("x_base", ctypes.c_uint32),
+        ("consumed_value", ctypes.c_uint32),
+        ("consumed_peer", ctypes.c_void_p),
+        ("y_peer_planes", ctypes.c_void_p),
+        ("y_peer_avail", ctypes.c_void_p),
+        ("y_base", ctypes.c_uint32),
+        ("consumed_wait", ctypes.c_uint32),
+        ("consumed", ctypes.c_void_p),
+        ("chunks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 5),
+    ]
+
+
 def make_desc(spec: RNNSpec) -> _Desc:
     return _Desc(
         CELLS[spec.cell], spec.layers, spec.dirs, spec.I, spec.hidden, spec.seq, spec.batch,
@@ -181,6 +202,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_profile_cells.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, fp, fp]
     lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.hs_rnn_forward_stage.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(StageLink), vp, sz, vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ABI_SYMBOLS[3:]:
         getattr(lib, name).restype = ctypes.c_int
@@ -469,6 +491,37 @@ class RNNExecutor:
                     ctypes.byref(desc), self.packed.data_ptr(), x_host.data_ptr(), ptr(h0), ptr(c0),
                     y.data_ptr(), hn.data_ptr(), ptr(cn), xd.data_ptr(), yd.data_ptr(), hnd.data_ptr(), ptr(cnd),
                     state.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), stream.cuda_stream,
+                ),
+            )
+        return y, hn, cn
+
+    def forward_stage(self, link: "StageLink", x=None, h0=None, c0=None, out=None):
+        """One layer-pipeline stage (``hs_rnn_forward_stage``): input from
+        ``link.x_planes`` (or ``x``), output shipped to the next stage through
+        ``link``; returns ``(y, h_n, c_n)`` of this stage's layers."""
+        self._require_resident()
+        s = self.spec
+        if x is not None:
+            if x.device != self.device or x.dtype != torch.float32 or not x.is_contiguous():
+                raise ValueError("x must be a contiguous float32 tensor on the executor's device")
+            if tuple(x.shape) != (s.seq, s.batch, s.I):
+                raise ValueError(f"x has shape {tuple(x.shape)}, expected {(s.seq, s.batch, s.I)}")
+        elif not link.x_planes:
+            raise ValueError("a stage needs x or link.x_planes")
+        state = (s.layers * s.dirs, s.batch, s.hidden)
+        self._check_dev("h0", h0, state)
+        self._check_dev("c0", c0 if s.cell == "lstm" else None, state)
+        y, hn, cn = out if out is not None else self.alloc_outputs()
+        ptr = lambda t: t.data_ptr() if t is not None else None
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            _check(
+                self.lib,
+                "hs_rnn_forward_stage",
+                self.lib.hs_rnn_forward_stage(
+                    ctypes.byref(self.desc), self.packed.data_ptr(), ptr(x), ptr(h0), ptr(c0),
+                    y.data_ptr(), hn.data_ptr(), ptr(cn), ctypes.byref(link), self.workspace.data_ptr(),
+                    self.workspace.numel(), stream.cuda_stream,
                 ),
             )
         return y, hn, cn
