@@ -343,8 +343,10 @@ def describe(spec) -> str:
 
 def run_pipeline(args, spec, world, rank, local, dev):
     """Layer pipeline over `world` GPUs: rank g owns
-    a contiguous layer range, hands [chunk, B, H] outputs to rank g+1 over
-    NCCL point-to-point (NVLink).  One timed step = `inflight` requests
+    a contiguous layer range and hands its output to rank g+1 — by default
+    as bf16 hi/lo planes copied GPU-to-GPU per chunk of `chunk` steps while
+    its last recurrence runs (--handoff peer), or as [chunk, B, H] NCCL
+    point-to-point sends between per-chunk stage forwards (--handoff nccl).  One timed step = `inflight` requests
     streamed through the pipeline (default: one per stage, so the pipeline
     is full in steady state); value = sequences/s of the whole pipeline."""
     import torch
@@ -356,8 +358,19 @@ def run_pipeline(args, spec, world, rank, local, dev):
 
     inflight = args.inflight or max(world, 1)
     weights = init_weights(spec, 0)
-    pipe = LayerPipeline(spec, weights, rank, world, args.chunk, lambda sp, w: RNNExecutor(sp, w, device=dev))
-    xs = [make_input(spec, 1 + r).pin_memory() for r in range(inflight)] if rank == 0 else [None] * inflight
+    if args.handoff == "peer":
+        # whole-sequence stage forwards; output planes copied GPU-to-GPU chunk
+        # by chunk (hs_rnn_forward_stage / parallel.PeerPipeline)
+        from paper_2307_11339_b200.parallel import PeerPipeline, stage_layers
+
+        l0, l1 = stage_layers(spec.layers, world, rank)
+        sspec = spec.with_(layers=l1 - l0, input=spec.I if rank == 0 else spec.hidden)
+        pipe = PeerPipeline(RNNExecutor(sspec, weights[l0:l1], device=dev), rank, world, chunk=args.chunk)
+        pipe.l0, pipe.l1, pipe.model = l0, l1, pipe.ex
+        xs = [make_input(spec, 1 + r).to(dev) for r in range(inflight)] if rank == 0 else [None] * inflight
+    else:
+        pipe = LayerPipeline(spec, weights, rank, world, args.chunk, lambda sp, w: RNNExecutor(sp, w, device=dev))
+        xs = [make_input(spec, 1 + r).pin_memory() for r in range(inflight)] if rank == 0 else [None] * inflight
 
     def barrier():
         if world > 1:
@@ -392,7 +405,11 @@ def run_pipeline(args, spec, world, rank, local, dev):
             "config": {"workload": f"{args.config}: {describe(spec)}, layer-pipelined", "mode": "pipeline",
                        "stages": world, "stage0_layers": [pipe.l0, pipe.l1] if rank == 0 else None,
                        "chunk": args.chunk, "requests_per_step": inflight, "algo": getattr(pipe.model, "algo", None),
-                       "parallelism": f"layer pipeline x{world} (NCCL P2P hand-off, no collective)"},
+                       "handoff": args.handoff,
+                       "parallelism": f"layer pipeline x{world} ("
+                                      + ("copy-engine GPU-to-GPU hand-off per chunk of steps, stream-ordered counters"
+                                         if args.handoff == "peer" else "NCCL P2P hand-off per chunk")
+                                      + ", no collective)"},
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -454,6 +471,9 @@ def main(argv=None):
     ap.add_argument("--mode", choices=["shard", "pipeline"], default="shard",
                     help="shard: N independent request shards (weak scaling); pipeline: layers split over N GPUs")
     ap.add_argument("--chunk", type=int, default=32, help="pipeline mode: timesteps per hand-off chunk")
+    ap.add_argument("--handoff", choices=["peer", "nccl"], default="peer",
+                    help="pipeline mode: peer = one stage forward per request with copy-engine GPU-to-GPU hand-off "
+                         "(hs_rnn_forward_stage); nccl = per-chunk stage forwards with NCCL isend/irecv (round 1)")
     ap.add_argument("--inflight", type=int, default=0, help="pipeline mode: requests per timed step (default N)")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="shard mode: split this many sequences over the N ranks (parallel.RequestShard, strong "

@@ -330,8 +330,10 @@ class PeerPipeline:
                 "x_avail": _share(self.x_avail) if self.x_avail is not None else None,
                 "consumed": _share(self.consumed) if self.consumed is not None else None}
         torch.cuda.synchronize(dev)
-        allv = [None] * world
-        dist.all_gather_object(allv, mine, group=group)
+        allv = [mine]
+        if world > 1:
+            allv = [None] * world
+            dist.all_gather_object(allv, mine, group=group)
         self.next_slots = self.next_avail = self.prev_consumed = None
         if rank < world - 1:
             nxt = allv[rank + 1]
