@@ -48,7 +48,8 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+    """SM clocks + throttle reasons during the timed region: NVML every 10 ms
+    (plus entry and exit) and nvidia-smi every 200 ms, merged."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
 
@@ -60,8 +61,10 @@ class ClockSampler:
 
     def __enter__(self):
         exe = shutil.which("nvidia-smi")
-        if not exe:
-            self._start_nvml()
+        # NVML readings at entry, every 10 ms and at exit: short timed regions
+        # (nvidia-smi's first line can take longer than the region) still get
+        # samples under load; nvidia-smi's stream is merged in when present
+        self._start_nvml()
         if exe:
             self.proc = subprocess.Popen(
                 [exe, f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
