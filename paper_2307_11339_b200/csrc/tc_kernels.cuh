@@ -657,6 +657,12 @@ inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, Tc
   a.S = S;
   a.RB = a.H / 32;
   a.Npad = pad16((a.B + 1) / 2);
+  // W_hh slice in TMEM (TS-mode MMAs) when it fits beside the two accumulators
+  static const char* wt_env = getenv("HS_W_TMEM");  // HS_W_TMEM=0: W_hh in shared memory (A/B)
+  a.whh_g[0] = reinterpret_cast<const uint16_t*>(whh[0]);
+  a.whh_g[1] = reinterpret_cast<const uint16_t*>(whh[a.D > 1 ? 1 : 0]);
+  a.w_tmem = !(wt_env && atoi(wt_env) == 0) && w_tmem_cols(a.H, S, NPL) <= 256 && a.Npad <= 64 &&
+             (a.H / S) % 64 == 0;
   CUtensorMap w0, w1, hm;
   int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);

@@ -66,7 +66,43 @@ struct TcRecurArgs {
   // direction: stamps[d*(T+1)] at the first step's start, stamps[d*(T+1)+s+1]
   // when step s's h is released (hs_rnn_profile_cells)
   unsigned long long* stamps;
+  // W_hh resident in TENSOR memory instead of shared memory (A operand of
+  // tcgen05.mma read from TMEM): in SS mode every M=128, K=16 MMA re-reads
+  // 4 KiB of W from shared memory, which paced the MMA phase of a step at
+  // ~75 cycles per instruction (c2 trace: 32 MMAs = 1.2 of 5.4 us)
+  const uint16_t* whh_g[2];     // per dir: packed planes [NPL][RB*128][H] (global)
+  int w_tmem;                   // 1 = load the CTA's slice into TMEM and run TS-mode MMAs
 };
+
+// TMEM columns of the CTA's W_hh slice (16-bit elements, two per column)
+__host__ __device__ inline int w_tmem_cols(int H, int S, int NPL) { return NPL * (H / S) / 2; }
+// The CTA's W_hh slice -> TMEM columns [wcol, wcol + w_tmem_cols): lane r =
+// MMA row r (warp w writes lanes 32*(w%4)..), the K elements of plane p at
+// columns p*KS/2 .. in order, the lower K index in the low 16 bits.  Warps
+// w and w+4 split the planes (NPL = 2) or the K halves (NPL = 1).
+__device__ __forceinline__ void load_w_tmem(const uint16_t* __restrict__ wg, size_t plane_elems, int H, int row0,
+                                            int k0, int KS, int NPL, uint32_t tmem_w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= 8) return;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = row0 + quarter * 32 + lane;
+  const int per = NPL * KS / 2;                   // elements this thread writes
+  const int p = NPL == 2 ? half : 0;
+  const int kb = NPL == 2 ? 0 : half * (KS / 2);  // first K element of this thread's part
+  const uint16_t* src = wg + (size_t)p * plane_elems + (size_t)row * H + k0 + kb;
+  const uint32_t col0 = (uint32_t)((p * KS + kb) / 2);
+  for (int e = 0; e < per; e += 32) {             // 32 elements = 16 columns per store
+    uint32_t r[16];
+    const uint4* v = reinterpret_cast<const uint4*>(src + e);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 u = __ldg(v + j);
+      r[4 * j] = u.x; r[4 * j + 1] = u.y; r[4 * j + 2] = u.z; r[4 * j + 3] = u.w;
+    }
+    ptx::tmem_st_32x32b_x16(tmem_w + ((uint32_t)(quarter * 32) << 16) + col0 + (uint32_t)(e / 2), r);
+  }
+  ptx::tmem_wait_st();
+}
 // timestep (row of xproj / y) of processing step `step` of direction d
 __device__ __forceinline__ int seg_time(const TcRecurArgs& a, int d, int step) {
   const int Tf = a.T_full ? a.T_full : a.T;

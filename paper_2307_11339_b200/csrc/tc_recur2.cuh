@@ -99,7 +99,9 @@ __global__ void __launch_bounds__(256, 1)
   const int GH = G * H;
   const int rstride = Np + 4;
   const uint32_t tcols_g = Np <= 32 ? 32 : Np <= 64 ? 64 : 128;
-  const uint32_t tcols = 2 * tcols_g;
+  // accumulators in columns [0, 2*tcols_g); W_hh (a.w_tmem) from column 256
+  const uint32_t wcol = 256u;
+  const uint32_t tcols = a.w_tmem ? 512u : 2 * tcols_g;
   constexpr int kCtrStride = kCtrStrideWords;
   const int nchunk_all = H / 64;
   unsigned int* ctr_g = a.counters + (size_t)grp * D * nchunk_all * kCtrStride;
@@ -130,13 +132,19 @@ __global__ void __launch_bounds__(256, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot + (uint32_t)(grp * tcols_g);
 
-  if (warp == 0 && ptx::elect_one()) {
+  if (a.w_tmem) {  // the CTA's W_hh slice into TMEM (all 8 warps), visible to the MMA issuer below
+    load_w_tmem(a.whh_g[d], (size_t)RB * 128 * H, H, rb * 128, q * KS, KS, NPL, *tmem_slot + wcol);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  } else if (warp == 0 && ptx::elect_one()) {
     ptx::mbar_arrive_expect_tx(w_full, (uint32_t)(NPL * nch * 128 * 128));
     for (int p = 0; p < NPL; ++p)
       for (int c = 0; c < nch; ++c)
         ptx::tma_load_3d(sW + ((size_t)p * nch + c) * 128 * 64, tmW, w_full, q * KS + c * 64, rb * 128, p);
   }
   __syncwarp();
+  const uint32_t tmem_w = *tmem_slot + wcol;
 
   // owner cells of this group: unit u_loc, group rows b = b0 + k*bstep
   const int u_loc = eg % UO;
@@ -219,20 +227,34 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
     } else if (sub == 1) {  // MMA issuer of this group
       if (ptx::elect_one()) {
-        if (s == 0) ptx::mbar_wait(w_full, 0);
-        else ptx::mbar_wait(tmem_free, (s - 1) & 1);
+        if (s == 0) {
+          if (!a.w_tmem) ptx::mbar_wait(w_full, 0);
+        } else {
+          ptx::mbar_wait(tmem_free, (s - 1) & 1);
+        }
         for (int c = 0; c < nch; ++c) {
           ptx::mbar_wait(&h_full[c], s & 1);
           ptx::tc_fence_after();
+          if (grp == 0 && c == 0) HS_TRACE(14);
+          if (grp == 0 && c == nch - 1) HS_TRACE(15);
           const __nv_bfloat16* wh = sW + (size_t)c * 128 * 64;
           const __nv_bfloat16* hh = sH + (size_t)c * Np * 64;
+          if (a.w_tmem) {  // A = W columns of (plane, chunk, kk): 8 columns per K=16
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
-                             (c | kk) != 0);
-            if (NPL == 2) {
-              const __nv_bfloat16* wl = wh + (size_t)nch * 128 * 64;
-              ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = ptx::sdesc_k_sw128(hh + kk * 16);
+              ptx::mma_bf16_ts(tmem, tmem_w + (uint32_t)(c * 32 + kk * 8), bd, idesc, (c | kk) != 0);
+              if (NPL == 2) ptx::mma_bf16_ts(tmem, tmem_w + (uint32_t)(KS / 2 + c * 32 + kk * 8), bd, idesc, 1);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
+                               (c | kk) != 0);
+              if (NPL == 2) {
+                const __nv_bfloat16* wl = wh + (size_t)nch * 128 * 64;
+                ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
+              }
             }
           }
         }

@@ -23,7 +23,9 @@ tr = np.fromfile(out, dtype=np.uint64).reshape(320, 64, 16).astype(np.int64)[:12
 T0, T1 = 2, 60
 ph = lambda i: tr[:, T0:T1, i]
 med = lambda v: np.median(v) / 1e3
-for name, a_, b_ in [("top -> chunk0 seen", 0, 1), ("chunk0 -> last chunk seen", 1, 12), ("last seen -> commit issued", 12, 2),
+for name, a_, b_ in [("top -> chunk0 seen", 0, 1), ("chunk0 -> last chunk seen", 1, 12),
+                     ("last seen -> chunk0 landed (MMA thr)", 12, 14), ("chunk0 -> last chunk landed", 14, 15),
+                     ("last landed -> commit issued", 15, 2),
                      ("commit -> acc seen (thr 64)", 2, 3), ("red_free wait", 3, 7), ("tmem ld + dsmem stores", 7, 8),
                      ("fence + arrives", 8, 4),
                      ("wait red_full", 4, 5), ("gates + h stores", 5, 6), ("-> release done", 6, 10)]:
