@@ -457,6 +457,27 @@ inline int max_coresident_ctas(int G, int NPL, int S, size_t smem) {
   return NPL == 2 ? max_coresident_ctas_t<3, 2>(S, smem) : max_coresident_ctas_t<3, 1>(S, smem);
 }
 
+// A CTA holding W_hh in TMEM allocates all 512 columns: two such CTAs on one
+// SM would block each other's allocation inside a persistent, co-dependent
+// grid.  Dynamic shared memory is padded past half an SM so the hardware
+// places one per SM; 0 = the grid would not fit that way (keep W in smem).
+inline size_t one_cta_per_sm(size_t smem, int ctas, int sms) {
+  constexpr size_t kHalf = 116 * 1024;  // > (228 KB per SM - 2 KB reserved) / 2
+  if (smem > kHalf) return smem;
+  return ctas <= sms ? kHalf + 1024 : 0;
+}
+
+// W_hh in TMEM for the resident single-group recurrence (tc_recur.cuh
+// load_w_tmem): the slice's NPL*KS/2 columns at column 256, the accumulator
+// (<= 256 columns) below.  HS_W_TMEM=0 keeps W_hh in shared memory (A/B).
+inline void set_w_tmem(TcRecurArgs& a, const __nv_bfloat16* const* whh, int S, int NPL, int nsw) {
+  static const char* env = getenv("HS_W_TMEM");
+  a.whh_g[0] = reinterpret_cast<const uint16_t*>(whh[0]);
+  a.whh_g[1] = reinterpret_cast<const uint16_t*>(whh[a.D > 1 ? 1 : 0]);
+  a.w_tmem = !(env && atoi(env) == 0) && nsw == 0 && w_tmem_cols(a.H, S, NPL) <= 256 && pad16(a.B) <= 256 &&
+             (a.H / S) % 64 == 0;
+}
+
 // persistent recurrences launch cooperatively (HS_COOP=0: plain cluster launch,
 // A/B only).  Nsight Compute fails cooperative cluster launches with
 // LaunchFailed; it replays one kernel at a time, so the occupancy check
@@ -538,7 +559,6 @@ inline int dispatch_cells(int G, int NPL, int cells, F&& f, std::string& err) {
 // One layer of recurrence (both directions).  W_hh planes for dir d at whh[d].
 inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, int sms,
                             cudaStream_t s, std::string& err) {
-  (void)sms;
   int nsw_try = 0;  // ring depth the limit is evaluated for
   auto limit = [&](int S_) -> int {
     const size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total;
@@ -562,12 +582,15 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   }
   a.S = S;
   a.RB = a.H / 32;
+  set_w_tmem(a, whh, S, NPL, nsw);
   CUtensorMap w0, w1, hm;
   int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D, a.Npad, err);
   if (rc) return rc;
-  const size_t smem = recur_layout(G, a.H, a.Npad, S, NPL, nsw).total;
+  size_t smem = recur_layout(G, a.H, a.Npad, S, NPL, nsw).total;
+  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) a.w_tmem = 0;
+  if (a.w_tmem) smem = one_cta_per_sm(smem, a.D * a.RB * S, sms);
   int cells = 1;
   while (cells * (kEpiThreads / (32 / S)) < a.Npad) cells *= 2;
   if (nsw) {  // streaming variant: instantiated for <= 4 cells per thread
@@ -668,7 +691,11 @@ inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, Tc
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * kNG, a.Npad, err);
   if (rc) return rc;
-  const size_t smem = recur2_layout(G, a.H, a.Npad, S, NPL).total;
+  size_t smem = recur2_layout(G, a.H, a.Npad, S, NPL).total;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_device()) != cudaSuccess) sms = 0;
+  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) a.w_tmem = 0;
+  if (a.w_tmem) smem = one_cta_per_sm(smem, a.D * a.RB * S, sms);
   int cells = 1;
   while (cells * (128 / (32 / S)) < a.Npad) cells *= 2;
   return dispatch_cells(G, NPL, cells, [&](auto g_, auto npl_, auto c_) -> int {

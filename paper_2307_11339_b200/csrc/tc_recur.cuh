@@ -272,7 +272,11 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   const CUtensorMap* tmW = d == 0 ? &tmW0 : &tmW1;
   const int GH = G * H;
   const int rstride = Npad + 4;
-  const uint32_t tcols = Npad <= 32 ? 32 : Npad <= 64 ? 64 : Npad <= 128 ? 128 : 256;
+  const uint32_t tcols_acc = Npad <= 32 ? 32 : Npad <= 64 ? 64 : Npad <= 128 ? 128 : 256;
+  // W_hh in TMEM (a.w_tmem, resident variant only): columns [256, 256 + NPL*KS/2)
+  const bool wt = NSW == 0 && a.w_tmem;
+  const uint32_t wcol = 256u;
+  const uint32_t tcols = wt ? 512u : tcols_acc;
   // readiness counters, one per 64-unit chunk of h (= 2 row blocks = 2S producer
   // CTAs), each on its own 128-B line
   constexpr int kCtrStride = kCtrStrideWords;
@@ -305,7 +309,12 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   const uint32_t tmem = *tmem_slot;
 
   // resident W_hh slice: NPL planes x nch chunks of [128 rows x 64 k]
-  if (NSW == 0 && warp == 0 && ptx::elect_one()) {
+  if (wt) {
+    load_w_tmem(a.whh_g[d], (size_t)RB * 128 * H, H, rb * 128, q * KS, KS, NPL, tmem + wcol);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  } else if (NSW == 0 && warp == 0 && ptx::elect_one()) {
     ptx::mbar_arrive_expect_tx(w_full, (uint32_t)(NPL * nch * 128 * 128));
     for (int p = 0; p < NPL; ++p)
       for (int c = 0; c < nch; ++c)
@@ -421,7 +430,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       __syncwarp();
     } else if (warp == 1) {
       if (ptx::elect_one()) {
-        if (NSW == 0 && s == 0) ptx::mbar_wait(w_full, 0);
+        if (NSW == 0 && s == 0 && !wt) ptx::mbar_wait(w_full, 0);
         if (s > 0) ptx::mbar_wait(tmem_free, (s - 1) & 1);  // every warp drained step s-1
         for (int c = 0; c < nch; ++c) {
           const int gi = s * nch + c, wslot = NSW ? gi % NSW : 0;
@@ -432,13 +441,22 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
           if (c == nch - 1) HS_TRACE(14);
           const __nv_bfloat16* wh = NSW ? sW + (size_t)wslot * NPL * 128 * 64 : sW + (size_t)c * 128 * 64;
           const __nv_bfloat16* hh = sH + (size_t)c * Npad * 64;
+          if (wt) {  // A = W columns of (plane, chunk, kk) in TMEM: 8 columns per K=16
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
-                             (c | kk) != 0);
-            if (NPL == 2) {  // + W_lo · h
-              const __nv_bfloat16* wl = wh + (size_t)(NSW ? 1 : nch) * 128 * 64;
-              ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = ptx::sdesc_k_sw128(hh + kk * 16);
+              ptx::mma_bf16_ts(tmem, tmem + wcol + (uint32_t)(c * 32 + kk * 8), bd, idesc, (c | kk) != 0);
+              if (NPL == 2) ptx::mma_bf16_ts(tmem, tmem + wcol + (uint32_t)(KS / 2 + c * 32 + kk * 8), bd, idesc, 1);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wh + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc,
+                               (c | kk) != 0);
+              if (NPL == 2) {  // + W_lo · h
+                const __nv_bfloat16* wl = wh + (size_t)(NSW ? 1 : nch) * 128 * 64;
+                ptx::mma_bf16_ss(tmem, ptx::sdesc_k_sw128(wl + kk * 16), ptx::sdesc_k_sw128(hh + kk * 16), idesc, 1);
+              }
             }
           }
           if (NSW) ptx::mma_commit(&wempty[wslot]);  // ring slot free once these MMAs have read it

@@ -175,6 +175,7 @@ inline int launch_wave(int G, int NPL, const WavePlan& p, const __nv_bfloat16* c
     TcRecurArgs& a = wa.rec.layer[l];
     a.S = S;
     a.RB = RB;
+    set_w_tmem(a, &whh[l], S, NPL, 0);
     rc = make_map3(&rm.w[l], whh[l], H, (uint64_t)RB * 128, 2, 128, err);
     if (!rc) rc = make_map3(&rm.h[l], a.hbuf, H, Npad, 3, Npad, err);
   }
