@@ -377,7 +377,7 @@ def run_pipeline(args, spec, world, rank, local, dev):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[dev.index]) if dist.get_backend() == "nccl" else dist.barrier()
 
     for _ in range(args.warmup):
         pipe.run_many(xs)
@@ -497,12 +497,20 @@ def main(argv=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HS_BENCH_ONE_DEVICE=1 (+ HS_BENCH_BACKEND=gloo): every rank on cuda:0 — a
+    # code-path check of the multi-rank bench on a one-GPU box, not a measurement
+    one_dev = os.environ.get("HS_BENCH_ONE_DEVICE") == "1"
+    gpu = 0 if one_dev else local
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        torch.cuda.set_device(gpu)
+        backend = os.environ.get("HS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{gpu}"))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
-    dev = torch.device(f"cuda:{local if world > 1 else 0}")
+    dev = torch.device(f"cuda:{gpu if world > 1 else 0}")
     if args.mode == "pipeline":
         return run_pipeline(args, spec, world, rank, local, dev)
 
@@ -529,7 +537,7 @@ def main(argv=None):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[dev.index]) if dist.get_backend() == "nccl" else dist.barrier()
 
     def max_over_ranks(v: float) -> float:
         if world == 1:
