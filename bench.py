@@ -573,7 +573,7 @@ def main(argv=None):
     # a stream of K requests through RNNServer.run_stream — every request's
     # H2D of x and D2H of y/h_n/c_n inside the timed region; request i+1's
     # upload overlaps request i's compute (two staging slots)
-    server = RNNServer(ex)
+    server = RNNServer(ex, slots=int(os.environ.get("HS_STREAM_SLOTS", "3")))
     req = InferenceRequest(x=x_host)
     server.run_stream([req] * 2)
     lat = [server.run(req).device_ms for _ in range(5)]  # single-request latency (sync)

@@ -78,7 +78,11 @@ typedef struct hs_rnn_desc {
   int32_t upload_chunks;  /* hs_rnn_forward_host: time chunks x is uploaded in (0 = 4).
                             1 suits request streams (x already uploaded during the
                             previous request); more chunks lower single-request latency */
-  int32_t reserved[6];
+  int32_t async_outputs;  /* hs_rnn_forward_host: 1 = the D2H copies of y / h_n / c_n are NOT
+                            joined into `stream`: the next request's compute may start while
+                            they drain; hs_rnn_outputs_ready() waits for them.  0 = all work,
+                            copies included, complete when `stream` reaches the call's end */
+  int32_t reserved[5];
 } hs_rnn_desc;
 
 /* ABI version of the loaded library (HS_RNN_ABI_VERSION). */
@@ -161,6 +165,13 @@ int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed,
                         void* y_host, void* hn_host, void* cn_host,
                         void* x_dev, void* y_dev, void* hn_dev, void* cn_dev, void* state_dev,
                         void* workspace, size_t ws_bytes, void* stream);
+
+/* Completion of an async_outputs hs_rnn_forward_host call whose host output
+ * buffer is `y_host` (the last such call on this thread and device): with
+ * `stream` non-NULL, `stream` waits for its output copies; with NULL the
+ * calling thread blocks until they are done.  A later forward that reuses
+ * the same device staging buffers waits for them by itself. */
+int hs_rnn_outputs_ready(const void* y_host, void* stream);
 
 /* Convenience: pack + forward (weights in PyTorch layout).  Needs
  * packed_size + workspace bytes of workspace. */

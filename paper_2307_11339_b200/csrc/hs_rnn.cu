@@ -417,6 +417,32 @@ int x_free_event(const void* x_dev, cudaEvent_t* ev, bool* seen) {
   return HS_OK;
 }
 
+// async_outputs forwards: per (device, device staging y buffer) the event
+// recorded after the call's output copies; the host buffer it drains into
+// keys hs_rnn_outputs_ready.  Per host thread, like the internal streams.
+struct DrainEntry { const void* y_dev; const void* y_host; int dev; cudaEvent_t ev; bool pending; };
+DrainEntry* drain_entry(const void* y_dev, const void* y_host, bool create) {
+  static thread_local DrainEntry cache[8] = {};
+  static thread_local int next = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  for (auto& e : cache)
+    if (e.ev && e.dev == dev && ((y_dev && e.y_dev == y_dev) || (!y_dev && e.y_host == y_host))) return &e;
+  if (!create) return nullptr;
+  DrainEntry& e = cache[next];
+  next = (next + 1) % 8;
+  if (e.ev && e.dev != dev) {
+    cudaEventDestroy(e.ev);
+    e.ev = nullptr;
+  }
+  if (!e.ev && cudaEventCreateWithFlags(&e.ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  e.y_dev = y_dev;
+  e.y_host = y_host;
+  e.dev = dev;
+  e.pending = false;
+  return &e;
+}
+
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValue32Fn wait_value_fn() {
   static WaitValue32Fn fn = nullptr;
@@ -1760,6 +1786,13 @@ int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void*
   float* yd = static_cast<float*>(y_dev);
   float* hnd = static_cast<float*>(hn_dev);
   float* cnd = static_cast<float*>(cn_dev);
+  // a previous async_outputs call that drained out of these staging buffers:
+  // its copies finish before this call's kernels overwrite them
+  if (DrainEntry* prev = drain_entry(yd, nullptr, false)) {
+    if (prev->pending) HS_CUDA(cudaStreamWaitEvent(s, prev->ev, 0));
+    prev->pending = false;
+  }
+  const bool async_out = desc->async_outputs != 0 && algo == HS_ALGO_TC;
   if (algo == HS_ALGO_TC) {
     Overlap ov;
     ov.x_host = static_cast<const float*>(x_host);
@@ -1768,6 +1801,19 @@ int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void*
     if ((rc = copy_stream(1, &ov.cs_out))) return rc;
     rc = forward_impl(m, algo, di, pl, packed, xd, h0d, c0d, yd, hnd, cnd, workspace, wl, s, nullptr, &ov);
     if (rc) return rc;
+    if (async_out) {
+      // the final states follow the y chunks on the copy stream, after the
+      // whole forward; the next request's work on `s` does not wait for them
+      if ((rc = join(s, ov.cs_out))) return rc;
+      HS_CUDA(cudaMemcpyAsync(hn_host, hnd, sbytes, cudaMemcpyDeviceToHost, ov.cs_out));
+      if (m.G == 4) HS_CUDA(cudaMemcpyAsync(cn_host, cnd, sbytes, cudaMemcpyDeviceToHost, ov.cs_out));
+      DrainEntry* e = drain_entry(yd, y_host, true);
+      if (!e) return fail(HS_ERR_CUDA, "cannot create the output-drain event");
+      e->y_host = y_host;
+      HS_CUDA(cudaEventRecord(e->ev, ov.cs_out));
+      e->pending = true;
+      return HS_OK;
+    }
     if ((rc = join(ov.cs_out, s))) return rc;  // y drained before the call's work on s completes
   } else {
     HS_CUDA(cudaMemcpyAsync(xd, x_host, xbytes, cudaMemcpyHostToDevice, s));
@@ -1777,6 +1823,18 @@ int hs_rnn_forward_host(const hs_rnn_desc* desc, const void* packed, const void*
   }
   HS_CUDA(cudaMemcpyAsync(hn_host, hnd, sbytes, cudaMemcpyDeviceToHost, s));
   if (m.G == 4) HS_CUDA(cudaMemcpyAsync(cn_host, cnd, sbytes, cudaMemcpyDeviceToHost, s));
+  return HS_OK;
+}
+
+int hs_rnn_outputs_ready(const void* y_host, void* stream) {
+  if (!y_host) return fail(HS_ERR_INVALID, "y_host must be non-NULL");
+  DrainEntry* e = drain_entry(nullptr, y_host, false);
+  if (!e) return HS_OK;  // no async_outputs call drained into this buffer on this thread
+  if (stream) {
+    HS_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->ev, 0));
+  } else {
+    HS_CUDA(cudaEventSynchronize(e->ev));
+  }
   return HS_OK;
 }
 

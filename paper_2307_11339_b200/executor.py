@@ -493,12 +493,15 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
             # host-produced final outputs -> device y / h_n / c_n
             torch.cuda.synchronize(dev)
             y = act_d[L - 1]
+            # host-produced rows of the output: one upload of the host mirror and
+            # one masked select instead of a copy per cell
+            mask = torch.zeros((T, 1, D * H), dtype=torch.bool)
             for v in range(n):
-                if sel[v] == GPU:
-                    continue
                 l, d, t, s = cells[v]
-                if l == L - 1:
-                    y[t, :, d * H:(d + 1) * H].copy_(act_h[l][t, :, d * H:(d + 1) * H])
+                if sel[v] != GPU and l == L - 1:
+                    mask[t, 0, d * H:(d + 1) * H] = True
+            if bool(mask.any()):
+                y = torch.where(mask.to(dev, non_blocking=True), act_h[L - 1].to(dev, non_blocking=True), y)
             hn = torch.empty((LD, B, H), device=dev)
             cn = torch.empty((LD, B, H), device=dev) if lstm else None
             for ld in range(LD):

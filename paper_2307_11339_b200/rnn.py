@@ -53,6 +53,7 @@ ABI_SYMBOLS = (
     "hs_rnn_forward",
     "hs_rnn_forward_host",
     "hs_rnn_forward_stage",
+    "hs_rnn_outputs_ready",
     "hs_rnn_run_cells",
 )
 
@@ -136,7 +137,8 @@ class _Desc(ctypes.Structure):
         ("dtype", ctypes.c_int32),
         ("algo", ctypes.c_int32),
         ("upload_chunks", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 6),
+        ("async_outputs", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 5),
     ]
 
 
@@ -203,6 +205,7 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_forward.argtypes = [pd, vp, pvp, pvp, pvp, pvp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_stage.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(StageLink), vp, sz, vp]
+    lib.hs_rnn_outputs_ready.argtypes = [vp, vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ABI_SYMBOLS[3:]:
         getattr(lib, name).restype = ctypes.c_int
@@ -451,7 +454,15 @@ class RNNExecutor:
         return tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory() if t is not None else None
                      for t in self.alloc_outputs())
 
-    def forward_host(self, x_host: torch.Tensor, h0=None, c0=None, out_host=None, staging=None, upload_chunks=0):
+    def outputs_ready(self, y_host: torch.Tensor, stream=None):
+        """Wait for the output copies of an ``async_outputs`` :meth:`forward_host`
+        into ``y_host``: make ``stream`` wait (GPU side), or block the calling
+        thread when ``stream`` is None (``hs_rnn_outputs_ready``)."""
+        _check(self.lib, "hs_rnn_outputs_ready",
+               self.lib.hs_rnn_outputs_ready(y_host.data_ptr(), stream.cuda_stream if stream is not None else None))
+
+    def forward_host(self, x_host: torch.Tensor, h0=None, c0=None, out_host=None, staging=None, upload_chunks=0,
+                     async_outputs=False):
         """End-to-end forward on host tensors (``hs_rnn_forward_host``): the
         H2D upload of ``x`` and the D2H download of ``y`` overlap the compute
         on the tensor-core path.  Host tensors should be pinned.  Returns the
@@ -482,6 +493,7 @@ class RNNExecutor:
         ptr = lambda t: t.data_ptr() if t is not None else None
         desc = make_desc(s)  # per call: concurrent callers never share a mutated descriptor
         desc.upload_chunks = int(upload_chunks)
+        desc.async_outputs = 1 if async_outputs else 0
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device)
             _check(

@@ -10,6 +10,7 @@ can be fed back into the cost model / serving simulator.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -17,6 +18,10 @@ import torch
 from .rnn import RNNExecutor
 
 __all__ = ["InferenceRequest", "InferenceResponse", "RNNServer", "register_model", "run"]
+
+# request streams drain each request's outputs off the compute stream
+# (hs_rnn_desc.async_outputs); HS_ASYNC_OUT=0 joins them in (A/B)
+_ASYNC_OUT = os.environ.get("HS_ASYNC_OUT", "1") != "0"
 
 
 @dataclass
@@ -42,7 +47,7 @@ class RNNServer:
     """Serves requests for one resident model.
 
     Device staging and pinned host outputs are preallocated in ``slots``
-    sets, so the request path allocates nothing.  Host requests go through
+    sets (default 3), so the request path allocates nothing.  Host requests go through
     ``hs_rnn_forward_host``: within a request, the H2D upload of x and the
     D2H download of y overlap the compute.  :meth:`run_stream` also overlaps
     requests with each other: request i+1's upload runs during request i's
@@ -50,7 +55,7 @@ class RNNServer:
     for the previous forward that used the same staging buffer).
     """
 
-    def __init__(self, executor: RNNExecutor, slots: int = 2):
+    def __init__(self, executor: RNNExecutor, slots: int = 3):
         self.ex = executor
         self.slots = max(1, slots)
         self.staging = [executor.alloc_staging() for _ in range(self.slots)]
@@ -64,7 +69,7 @@ class RNNServer:
         if tuple(req.x.shape) != (s.seq, s.batch, s.I):
             raise ValueError(f"request x has shape {tuple(req.x.shape)}, model expects {(s.seq, s.batch, s.I)}")
 
-    def _submit(self, req: InferenceRequest, slot: int, upload_chunks: int = 0) -> tuple[int, int]:
+    def _submit(self, req: InferenceRequest, slot: int, upload_chunks: int = 0, async_outputs: bool = False) -> tuple[int, int]:
         """Enqueue one request on the current stream; returns (h2d, d2h) bytes."""
         ex = self.ex
         staging = self.staging[slot]
@@ -72,7 +77,8 @@ class RNNServer:
         if req.x.device.type == "cpu":
             h0 = req.h0.to(torch.float32).contiguous() if req.h0 is not None else None
             c0 = req.c0.to(torch.float32).contiguous() if req.c0 is not None else None
-            ex.forward_host(req.x.to(torch.float32).contiguous(), h0, c0, out_host=host_outs, staging=staging, upload_chunks=upload_chunks)
+            ex.forward_host(req.x.to(torch.float32).contiguous(), h0, c0, out_host=host_outs, staging=staging,
+                            upload_chunks=upload_chunks, async_outputs=async_outputs)
             h2d = sum(t.numel() * t.element_size() for t in (req.x, h0, c0) if t is not None)
         else:
             dev = ex.device
@@ -112,6 +118,9 @@ class RNNServer:
 
         def finish(slot):
             done[slot].synchronize()
+            # host requests drain their outputs off the stream (async_outputs):
+            # wait for this slot's copies, not for the requests behind it
+            self.ex.outputs_ready(self.host_outs[slot][0])
             i, h2d, d2h = pending[slot]
             y, hn, cn = self.host_outs[slot]
             if consume is not None:
@@ -125,7 +134,7 @@ class RNNServer:
             if pending[slot] is not None:
                 finish(slot)
             # in a stream the upload overlaps the previous request: one chunk
-            h2d, d2h = self._submit(req, slot, upload_chunks=1 if i else 0)
+            h2d, d2h = self._submit(req, slot, upload_chunks=1 if i else 0, async_outputs=_ASYNC_OUT)
             h2d_total += h2d
             d2h_total += d2h
             ev = done[slot] or torch.cuda.Event()

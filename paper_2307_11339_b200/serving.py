@@ -415,6 +415,8 @@ class ResidencyServer:
     (default: :func:`slo_from_latency` of its measured warm latency).
     """
 
+    SLOTS = 2  # request staging sets per resident model (requests here are served one at a time)
+
     def __init__(self, models: dict, capacity_mb: float, policy: str = "lru", slo_ms: dict | None = None,
                  inputs: dict | None = None):
         import torch
@@ -441,7 +443,7 @@ class ResidencyServer:
             state = st.layers * st.dirs * st.batch * st.hidden * 4
             staging = (st.seq * st.batch * st.I * 4 + st.seq * st.batch * st.dirs * st.hidden * 4
                        + state * (2 if st.cell == "lstm" else 1) + 2 * state)
-            self.footprint_mb[k] = (ex.packed_bytes() + ex.workspace_bytes() + 2 * staging) / MB
+            self.footprint_mb[k] = (ex.packed_bytes() + ex.workspace_bytes() + self.SLOTS * staging) / MB
             self.weights_mb[k] = ex.packed_bytes() / MB
             if self.footprint_mb[k] > self.capacity_mb:
                 raise ScenarioError(f"model {k} footprint {self.footprint_mb[k]} MB exceeds capacity {capacity_mb} MB")
@@ -469,7 +471,7 @@ class ResidencyServer:
 
         def go():
             ex.load()
-            self._servers[mid] = self._RNNServer(ex)
+            self._servers[mid] = self._RNNServer(ex, slots=self.SLOTS)
 
         return self._timed(go)
 
