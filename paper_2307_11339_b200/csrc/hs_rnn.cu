@@ -431,6 +431,9 @@ DrainEntry* drain_entry(const void* y_dev, const void* y_host, bool create) {
   if (!create) return nullptr;
   DrainEntry& e = cache[next];
   next = (next + 1) % 8;
+  // an evicted entry may still guard in-flight copies out of its staging
+  // buffers: wait for them rather than forget them
+  if (e.ev && e.pending) cudaEventSynchronize(e.ev);
   if (e.ev && e.dev != dev) {
     cudaEventDestroy(e.ev);
     e.ev = nullptr;

@@ -2,7 +2,8 @@
 (racecheck / synccheck / memcheck): the two-group recurrence at c2 width
 (B=64) with the dynamic next-layer K1, the layer-wave fused kernel at c3
 width, the W-streaming recurrence at c4 width (H=2048), the batch-sliced bf16
-path at c5 width, and the host-buffer request stream (request overlap)."""
+path at c5 width, the host-buffer request stream (request overlap, async
+output drain) and two layer-pipeline stages (stream-ordered peer hand-off)."""
 import sys
 from pathlib import Path
 
@@ -29,6 +30,28 @@ for name, spec in CASES:
 if not only or "stream" in only:
     spec = RNNSpec("lstm", 2, 1024, 6, 64, algo="tc")  # even layer count: request overlap on
     srv = RNNServer(RNNExecutor(spec, init_weights(spec)))
-    srv.run_stream([InferenceRequest(x=make_input(spec, 1 + i).pin_memory()) for i in range(3)])
+    srv.run_stream([InferenceRequest(x=make_input(spec, 1 + i).pin_memory()) for i in range(4)])  # async output drain
     torch.cuda.synchronize()
     print("ok request stream", flush=True)
+if not only or "stage" in only:
+    # two pipeline stages in one process, producer enqueued first (hs_rnn_forward_stage)
+    from paper_2307_11339_b200.parallel import stage_link_values
+    from paper_2307_11339_b200.rnn import StageLink
+
+    spec = RNNSpec("lstm", 2, 256, 8, 16, algo="tc")
+    w = init_weights(spec)
+    e0 = RNNExecutor(spec.with_(layers=1), w[:1])
+    e1 = RNNExecutor(spec.with_(layers=1, input=spec.hidden), w[1:])
+    T, B, H = spec.seq, spec.batch, spec.hidden
+    slots = torch.zeros((2, 2, T * B, H), dtype=torch.bfloat16, device="cuda")
+    avail = torch.zeros(1, dtype=torch.int32, device="cuda")
+    consumed = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for r in range(2):
+        v0, v1 = stage_link_values(r, T, 0, 2), stage_link_values(r, T, 1, 2)
+        e0.forward_stage(StageLink(y_peer_planes=slots[r % 2].data_ptr(), y_peer_avail=avail.data_ptr(),
+                                   y_base=v0["y_base"], consumed=consumed.data_ptr(),
+                                   consumed_wait=v0["consumed_wait"], chunks=2), x=make_input(spec, r).cuda())
+        e1.forward_stage(StageLink(x_planes=slots[r % 2].data_ptr(), x_avail=avail.data_ptr(), x_base=v1["x_base"],
+                                   consumed_peer=consumed.data_ptr(), consumed_value=v1["consumed_value"], chunks=2))
+    torch.cuda.synchronize()
+    print("ok pipeline stages", flush=True)
