@@ -1219,7 +1219,11 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
           HS_CUDA(cudaMemsetAsync(hbuf, 0, 3 * (size_t)m.D * 2 * pad16(m.B) * m.H * 2, s));
           HS_CUDA(cudaMemsetAsync(counters, 0, 128 * 128, s));
         }
-        rc = recurrence_layer(m.G, NPL, whh, sa, di.sms, s, g_err);
+        // a slice of >= 64 sequences runs as two batch-half chains too (W_hh in
+        // TMEM where the shared-memory layout does not fit, e.g. c5's slices)
+        const bool two_slice = (two_env ? atoi(two_env) == 1 : bn >= 64) && choose_split2(m.G, m.H, bn, m.D, NPL) > 0;
+        rc = two_slice ? recurrence_layer2(m.G, NPL, whh, sa, s, g_err)
+                       : recurrence_layer(m.G, NPL, whh, sa, di.sms, s, g_err);
         if (rc) return rc;
       }
     }
@@ -1542,7 +1546,7 @@ int hs_rnn_plan(const hs_rnn_desc* desc, int32_t* info) {
     const int Bs = hs::tc::batch_slice(m.G, m.H, m.B, m.D, NPL);
     int nsw = 0;
     info[1] = hs::tc::plan_split(m.G, m.H, Bs, m.D, NPL, hs::tc::static_cta_limit, &nsw);
-    info[2] = nsw;
+    info[2] = nsw > 0 ? nsw : 0;  // W ring depth (kTmemW = resident in tensor memory: 0)
     info[3] = Bs ? (m.B + Bs - 1) / Bs : 0;
     const hs::tc::WavePlan wp = wave_split(m);
     if (wp.S) {  // layer wavefront: K-split of the wave's recurrences, CTAs per SM

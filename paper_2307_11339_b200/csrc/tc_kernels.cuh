@@ -43,19 +43,29 @@ inline int choose_split(int G, int H, int B, int D, int NPL, Limit max_ctas, int
     if (H % (64 * S)) continue;
     const RecurLayout L = recur_layout(G, H, Npad, S, NPL, nsw);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
+    // W_hh in TMEM: its NPL*KS/2 columns at column 256 beside an accumulator of <= 256
+    if (nsw == kTmemW && (w_tmem_cols(H, S, NPL) > 256 || Npad > 256)) continue;
     if ((Npad + 8 * S - 1) / (8 * S) > RMAXCELLS) continue;
-    if (nsw && (Npad + 8 * S - 1) / (8 * S) > 4) continue;  // streaming variant: <= 4 cells per thread
+    // streaming and TMEM-resident variants: <= 4 cells per thread (8 spill: c5 at 96 rows ran 16.7 vs 7.5 us/step)
+    if (nsw != 0 && (Npad + 8 * S - 1) / (8 * S) > 4) continue;
     if (D * RB * S > max_ctas(S)) continue;
     best = S;  // increasing S -> larger grid; keep the largest that fits
   }
   return best;
 }
 
-// Resident W_hh when possible, else the W-streaming variant.  *nsw = ring depth (0 = resident).
+// Resident W_hh when possible — in shared memory, else in tensor memory (the
+// shared-memory layout then holds no W, which fits c5's batch-64 bf16 slices
+// and lets larger slices in) — else the W-streaming variant.
+// *nsw = 0 (smem-resident), kTmemW (TMEM-resident) or the ring depth.
 template <typename Limit>
 inline int plan_split(int G, int H, int B, int D, int NPL, Limit max_ctas, int* nsw) {
   int S = choose_split(G, H, B, D, NPL, max_ctas, 0);
   *nsw = 0;
+  if (!S) {
+    S = choose_split(G, H, B, D, NPL, max_ctas, kTmemW);
+    *nsw = S ? kTmemW : 0;
+  }
   if (!S) {
     S = choose_split(G, H, B, D, NPL, max_ctas, kSW);
     *nsw = S ? kSW : 0;
@@ -561,7 +571,8 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
                             cudaStream_t s, std::string& err) {
   int nsw_try = 0;  // ring depth the limit is evaluated for
   auto limit = [&](int S_) -> int {
-    const size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total;
+    size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total;
+    if (nsw_try == kTmemW && sm_ < 117 * 1024) sm_ = 117 * 1024;  // padded to one CTA per SM (see one_cta_per_sm)
     return max_coresident_ctas(G, NPL, S_, sm_);
   };
   int nsw = 0;
@@ -569,6 +580,12 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   int S = force_sw ? 0 : choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
   static const char* force_s0 = getenv("HS_FORCE_S");  // experiments: cap the K-split
   if (S && force_s0 && atoi(force_s0) > 0 && atoi(force_s0) < S) S = atoi(force_s0);
+  bool tmem_only = false;  // W_hh fits on chip only in TMEM (no shared-memory copy)
+  if (!S && !force_sw) {
+    nsw_try = kTmemW;
+    S = choose_split(G, a.H, a.B, a.D, NPL, limit, kTmemW);
+    tmem_only = S > 0;
+  }
   if (!S) {
     nsw_try = kSW;
     S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);
@@ -583,13 +600,21 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
   a.S = S;
   a.RB = a.H / 32;
   set_w_tmem(a, whh, S, NPL, nsw);
+  if (tmem_only) a.w_tmem = 1;  // the layout has no shared-memory W (HS_W_TMEM=0 cannot apply)
   CUtensorMap w0, w1, hm;
   int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D, a.Npad, err);
   if (rc) return rc;
-  size_t smem = recur_layout(G, a.H, a.Npad, S, NPL, nsw).total;
-  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) a.w_tmem = 0;
+  size_t smem = recur_layout(G, a.H, a.Npad, S, NPL, nsw).total;  // with W in smem: >= the kernel's TMEM layout
+  if (tmem_only) smem = recur_layout(G, a.H, a.Npad, S, NPL, kTmemW).total;
+  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) {
+    if (tmem_only) {
+      err = "TMEM-resident recurrence needs one CTA per SM";
+      return 3;
+    }
+    a.w_tmem = 0;
+  }
   if (a.w_tmem) smem = one_cta_per_sm(smem, a.D * a.RB * S, sms);
   int cells = 1;
   while (cells * (kEpiThreads / (32 / S)) < a.Npad) cells *= 2;
@@ -612,7 +637,9 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
 
 // ------------------------------------------- two-group recurrence (tc_recur2.cuh)
 // K-split for two batch halves per CTA; 0 = infeasible.
-inline int choose_split2(int G, int H, int B, int D, int NPL) {
+// With wtmem the layout holds no W_hh (it lives in TMEM): bidirectional
+// batch-64 slices (c5) fit at S=2, which the shared-memory layout does not.
+inline int choose_split2(int G, int H, int B, int D, int NPL, bool wtmem) {
   if (B < 2 || H % 64) return 0;
   const int Np = pad16((B + 1) / 2);
   if (Np > 64) return 0;
@@ -620,13 +647,26 @@ inline int choose_split2(int G, int H, int B, int D, int NPL) {
   int best = 0;
   for (int S = 1; S <= 8; S *= 2) {
     if (H % (64 * S)) continue;
-    const Recur2Layout L = recur2_layout(G, H, Np, S, NPL);
+    const Recur2Layout L = recur2_layout(G, H, Np, S, NPL, wtmem);
     if (L.nch > RMAXCH || L.total > kSmemMax) continue;
+    if (wtmem && w_tmem_cols(H, S, NPL) > 256) continue;
     if ((Np + (128 / (32 / S)) - 1) / (128 / (32 / S)) > 4) continue;  // <= 4 cells per thread
     if (D * RB * S > static_cta_limit(S)) continue;
     best = S;
   }
   return best;
+}
+// K-split of the two-group recurrence, W_hh in shared memory when that fits
+// (*tmem_only = false), else in tensor memory; 0 = infeasible.
+inline int choose_split2(int G, int H, int B, int D, int NPL, bool* tmem_only = nullptr) {
+  int S = choose_split2(G, H, B, D, NPL, false);
+  bool t = false;
+  if (!S) {
+    S = choose_split2(G, H, B, D, NPL, true);
+    t = S > 0;
+  }
+  if (tmem_only) *tmem_only = t;
+  return S;
 }
 
 template <int G, int NPL, int CELLS>
@@ -672,7 +712,8 @@ inline int launch_recur2(const CUtensorMap& w0, const CUtensorMap& w1, const CUt
 // a.B = full batch; a.Npad is set to the per-group padding; a.S / a.RB filled in.
 inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, TcRecurArgs& a, cudaStream_t s,
                              std::string& err) {
-  const int S = choose_split2(G, a.H, a.B, a.D, NPL);
+  bool tmem_only = false;
+  const int S = choose_split2(G, a.H, a.B, a.D, NPL, &tmem_only);
   if (!S) {
     err = "no feasible two-group split";
     return 3;
@@ -684,17 +725,23 @@ inline int recurrence_layer2(int G, int NPL, const __nv_bfloat16* const* whh, Tc
   static const char* wt_env = getenv("HS_W_TMEM");  // HS_W_TMEM=0: W_hh in shared memory (A/B)
   a.whh_g[0] = reinterpret_cast<const uint16_t*>(whh[0]);
   a.whh_g[1] = reinterpret_cast<const uint16_t*>(whh[a.D > 1 ? 1 : 0]);
-  a.w_tmem = !(wt_env && atoi(wt_env) == 0) && w_tmem_cols(a.H, S, NPL) <= 256 && a.Npad <= 64 &&
-             (a.H / S) % 64 == 0;
+  a.w_tmem = (tmem_only || !(wt_env && atoi(wt_env) == 0)) && w_tmem_cols(a.H, S, NPL) <= 256 &&
+             a.Npad <= 64 && (a.H / S) % 64 == 0;
   CUtensorMap w0, w1, hm;
   int rc = make_map3(&w0, whh[0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&w1, whh[a.D > 1 ? 1 : 0], a.H, (uint64_t)a.RB * 128, 2, 128, err);
   if (!rc) rc = make_map3(&hm, a.hbuf, a.H, a.Npad, (uint64_t)3 * a.D * kNG, a.Npad, err);
   if (rc) return rc;
-  size_t smem = recur2_layout(G, a.H, a.Npad, S, NPL).total;
+  size_t smem = recur2_layout(G, a.H, a.Npad, S, NPL, tmem_only).total;
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_device()) != cudaSuccess) sms = 0;
-  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) a.w_tmem = 0;
+  if (a.w_tmem && one_cta_per_sm(smem, a.D * a.RB * S, sms) == 0) {
+    if (tmem_only) {
+      err = "TMEM-resident two-group recurrence needs one CTA per SM";
+      return 3;
+    }
+    a.w_tmem = 0;
+  }
   if (a.w_tmem) smem = one_cta_per_sm(smem, a.D * a.RB * S, sms);
   int cells = 1;
   while (cells * (128 / (32 / S)) < a.Npad) cells *= 2;
@@ -718,9 +765,15 @@ inline int recurrence_ctas(int G, int NPL, const TcRecurArgs& a, bool two) {
   }
   int nsw_try = 0;
   auto limit = [&](int S_) -> int {
-    return max_coresident_ctas(G, NPL, S_, recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total);
+    size_t sm_ = recur_layout(G, a.H, pad16(a.B), S_, NPL, nsw_try).total;
+    if (nsw_try == kTmemW && sm_ < 117 * 1024) sm_ = 117 * 1024;
+    return max_coresident_ctas(G, NPL, S_, sm_);
   };
   int S = choose_split(G, a.H, a.B, a.D, NPL, limit, 0);
+  if (!S) {
+    nsw_try = kTmemW;
+    S = choose_split(G, a.H, a.B, a.D, NPL, limit, kTmemW);
+  }
   if (!S) {
     nsw_try = kSW;
     S = choose_split(G, a.H, a.B, a.D, NPL, limit, kSW);

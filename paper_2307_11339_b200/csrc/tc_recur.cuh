@@ -176,15 +176,17 @@ struct RecurLayout {
   size_t w_off, h_off, red_off, stage_off, bar_off, total;
 };
 
-// nsw = 0: the CTA's W_hh slice is resident (NPL planes x nch chunks);
+// nsw = 0: the CTA's W_hh slice is resident in shared memory (NPL planes x
+// nch chunks); nsw = kTmemW: resident in tensor memory, no shared-memory copy;
 // nsw > 0: W_hh does not fit on chip and streams through an nsw-stage ring of
 // [NPL planes x 128 rows x 64 k] chunks, re-read from L2 every step.
+constexpr int kTmemW = -1;
 __host__ __device__ inline RecurLayout recur_layout(int G, int H, int Npad, int S, int NPL, int nsw = 0) {
   RecurLayout L;
   const int KS = H / S;
   L.nch = KS / 64;
   size_t off = 0;
-  L.w_off = off;   off += (size_t)NPL * (nsw ? nsw : L.nch) * 128 * 128;
+  L.w_off = off;   off += nsw < 0 ? 0 : (size_t)NPL * (nsw ? nsw : L.nch) * 128 * 128;
   L.h_off = off;   off += (size_t)L.nch * Npad * 128;  // one h plane
   L.red_off = off; off += (size_t)G * 32 * (Npad + 4) * 4;
   // outgoing partials for the S-1 peers, laid out like their destination regions
@@ -246,7 +248,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 atoms need 1024-B alignment
   signal_started(a);
   const int H = a.H, B = a.B, Npad = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
-  const RecurLayout L = recur_layout(G, H, Npad, S, NPL, NSW);
+  const RecurLayout L = recur_layout(G, H, Npad, S, NPL, NSW == 0 && a.w_tmem ? kTmemW : NSW);
   const int nch = L.nch;
   const int KS = H / S;
   const int UO = 32 / S;  // units finished by each rank

@@ -33,13 +33,13 @@ struct Recur2Layout {
   size_t h_group, red_group, stage_group;  // bytes per group
 };
 
-// Np = padded rows of ONE group
-__host__ __device__ inline Recur2Layout recur2_layout(int G, int H, int Np, int S, int NPL) {
+// Np = padded rows of ONE group; wtmem: W_hh in tensor memory (no smem copy)
+__host__ __device__ inline Recur2Layout recur2_layout(int G, int H, int Np, int S, int NPL, bool wtmem = false) {
   Recur2Layout L;
   const int KS = H / S;
   L.nch = KS / 64;
   size_t off = 0;
-  L.w_off = off;   off += (size_t)NPL * L.nch * 128 * 128;
+  L.w_off = off;   off += wtmem ? 0 : (size_t)NPL * L.nch * 128 * 128;
   L.h_group = (size_t)L.nch * Np * 128;
   L.h_off = off;   off += kNG * L.h_group;
   L.red_group = (size_t)G * 32 * (Np + 4) * 4;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, 1)
   // a.B = total batch, a.Npad = padded rows of one group (Bh = ceil(B/2) rows each)
   const int H = a.H, B = a.B, Np = a.Npad, T = a.T, D = a.D, S = a.S, RB = a.RB;
   const int Bh = (B + 1) / 2;
-  const Recur2Layout L = recur2_layout(G, H, Np, S, NPL);
+  const Recur2Layout L = recur2_layout(G, H, Np, S, NPL, a.w_tmem != 0);
   const int nch = L.nch;
   const int KS = H / S;
   const int UO = 32 / S;
