@@ -477,6 +477,11 @@ inline size_t one_cta_per_sm(size_t smem, int ctas, int sms) {
   return ctas <= sms ? kHalf + 1024 : 0;
 }
 
+inline const char* wt_env0() {
+  static const char* env = getenv("HS_W_TMEM");
+  return env;
+}
+
 // W_hh in TMEM for the resident single-group recurrence (tc_recur.cuh
 // load_w_tmem): the slice's NPL*KS/2 columns at column 256, the accumulator
 // (<= 256 columns) below.  HS_W_TMEM=0 keeps W_hh in shared memory (A/B).
@@ -616,6 +621,16 @@ inline int recurrence_layer(int G, int NPL, const __nv_bfloat16* const* whh, TcR
     a.w_tmem = 0;
   }
   if (a.w_tmem) smem = one_cta_per_sm(smem, a.D * a.RB * S, sms);
+  // W-streaming: keep as many chunks of the slice in TMEM as fit after the
+  // accumulator (c4: 7 of 16 per step never cross the ring); HS_W_TMEM=0: none
+  a.w_tmem_chunks = 0;
+  if (nsw > 0 && !(wt_env0() && atoi(wt_env0()) == 0)) {
+    const int acc = a.Npad <= 32 ? 32 : a.Npad <= 64 ? 64 : a.Npad <= 128 ? 128 : 256;
+    const int nch = (a.H / S) / 64;
+    int n = (512 - acc) / (NPL * 32);
+    if (n >= nch) n = nch - 1;
+    if (n > 0 && one_cta_per_sm(smem, a.D * a.RB * S, sms) == smem) a.w_tmem_chunks = n;
+  }
   int cells = 1;
   while (cells * (kEpiThreads / (32 / S)) < a.Npad) cells *= 2;
   if (nsw) {  // streaming variant: instantiated for <= 4 cells per thread

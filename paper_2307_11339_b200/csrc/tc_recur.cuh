@@ -72,6 +72,7 @@ struct TcRecurArgs {
   // ~75 cycles per instruction (c2 trace: 32 MMAs = 1.2 of 5.4 us)
   const uint16_t* whh_g[2];     // per dir: packed planes [NPL][RB*128][H] (global)
   int w_tmem;                   // 1 = load the CTA's slice into TMEM and run TS-mode MMAs
+  int w_tmem_chunks;            // W-streaming variant: chunks [0, n) of the slice stay in TMEM, the rest stream
 };
 
 // TMEM columns of the CTA's W_hh slice (16-bit elements, two per column)
@@ -278,7 +279,10 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   // W_hh in TMEM (a.w_tmem, resident variant only): columns [256, 256 + NPL*KS/2)
   const bool wt = NSW == 0 && a.w_tmem;
   const uint32_t wcol = 256u;
-  const uint32_t tcols = wt ? 512u : tcols_acc;
+  // W-streaming variant: the first `nres` chunks (both planes) stay in TMEM
+  // after the accumulator, only the rest cross the ring each step
+  const int nres = NSW ? a.w_tmem_chunks : 0;
+  const uint32_t tcols = (wt || nres) ? 512u : tcols_acc;
   // readiness counters, one per 64-unit chunk of h (= 2 row blocks = 2S producer
   // CTAs), each on its own 128-B line
   constexpr int kCtrStride = kCtrStrideWords;
@@ -324,16 +328,41 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
   }
   __syncwarp();
 
+  if (nres) {  // resident part of the streamed slice: chunk c plane p at column tcols_acc + (c*NPL + p)*32
+    const int quarter = warp & 3, half = warp >> 2, row = rb * 128 + quarter * 32 + lane;
+    if (warp < 8) {
+      for (int i = half; i < nres * NPL; i += 2) {
+        const int c = i / NPL, p = i % NPL;
+        const uint16_t* src = a.whh_g[d] + (size_t)p * RB * 128 * H + (size_t)row * H + q * KS + c * 64;
+        for (int e = 0; e < 64; e += 32) {
+          uint32_t r[16];
+          const uint4* v = reinterpret_cast<const uint4*>(src + e);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 u = __ldg(v + j);
+            r[4 * j] = u.x; r[4 * j + 1] = u.y; r[4 * j + 2] = u.z; r[4 * j + 3] = u.w;
+          }
+          ptx::tmem_st_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + tcols_acc + (uint32_t)(i * 32 + e / 2), r);
+        }
+      }
+      ptx::tmem_wait_st();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
   // streaming variant: warp 8 keeps the W ring NSW chunks ahead of the MMAs.
-  // Ring item gi = s*nch + c holds chunk c (the same weights every step).
-  const int total_items = T * nch;
+  // Ring item gi = s*nstream + (c - nres) holds streamed chunk c (the same
+  // weights every step).
+  const int nstream = nch - nres;
+  const int total_items = T * nstream;
   int w_next = 0;  // next ring item to load (warp 8 lane 0)
   const uint64_t pol_w = ptx::policy_evict_last();
   const uint64_t pol_s = ptx::policy_evict_first();
   const bool hint_s = (a.l2_hints & kL2HintStream) != 0;
   auto w_produce_until = [&](int last_item) {
     for (; w_next <= last_item && w_next < total_items; ++w_next) {
-      const int slot = w_next % NSW, c = w_next % nch;
+      const int slot = w_next % NSW, c = nres + w_next % nstream;
       if (w_next >= NSW) ptx::mbar_wait(&wempty[slot], ((w_next / NSW) - 1) & 1);
       ptx::mbar_arrive_expect_tx(&wfull[slot], (uint32_t)(NPL * 128 * 128));
       for (int p = 0; p < NPL; ++p) {
@@ -428,15 +457,16 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       __syncwarp();
     } else if (NSW && warp == 8) {
       // keep the W ring NSW items ahead: this step's chunks, then the next step's first NSW
-      if (lane == 0) w_produce_until((s + 1) * nch + NSW - 1);
+      if (lane == 0) w_produce_until((s + 1) * nstream + NSW - 1);
       __syncwarp();
     } else if (warp == 1) {
       if (ptx::elect_one()) {
         if (NSW == 0 && s == 0 && !wt) ptx::mbar_wait(w_full, 0);
         if (s > 0) ptx::mbar_wait(tmem_free, (s - 1) & 1);  // every warp drained step s-1
         for (int c = 0; c < nch; ++c) {
-          const int gi = s * nch + c, wslot = NSW ? gi % NSW : 0;
-          if (NSW) ptx::mbar_wait(&wfull[wslot], (gi / NSW) & 1);
+          const bool in_tmem = c < nres;  // W-streaming variant: resident chunk, no ring slot
+          const int gi = s * nstream + (c - nres), wslot = NSW && !in_tmem ? gi % NSW : 0;
+          if (NSW && !in_tmem) ptx::mbar_wait(&wfull[wslot], (gi / NSW) & 1);
           ptx::mbar_wait(&h_full[c], s & 1);
           ptx::tc_fence_after();
           if (c == 0) HS_TRACE(15);
@@ -450,6 +480,14 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
               ptx::mma_bf16_ts(tmem, tmem + wcol + (uint32_t)(c * 32 + kk * 8), bd, idesc, (c | kk) != 0);
               if (NPL == 2) ptx::mma_bf16_ts(tmem, tmem + wcol + (uint32_t)(KS / 2 + c * 32 + kk * 8), bd, idesc, 1);
             }
+          } else if (in_tmem) {  // resident chunk of the streamed slice
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = ptx::sdesc_k_sw128(hh + kk * 16);
+              const uint32_t wc = tmem + tcols_acc + (uint32_t)(c * NPL * 32 + kk * 8);
+              ptx::mma_bf16_ts(tmem, wc, bd, idesc, (c | kk) != 0);
+              if (NPL == 2) ptx::mma_bf16_ts(tmem, wc + 32u, bd, idesc, 1);
+            }
           } else {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
@@ -461,7 +499,7 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
               }
             }
           }
-          if (NSW) ptx::mma_commit(&wempty[wslot]);  // ring slot free once these MMAs have read it
+          if (NSW && !in_tmem) ptx::mma_commit(&wempty[wslot]);  // ring slot free once these MMAs have read it
         }
         ptx::mma_commit(acc_full);
         HS_TRACE(2);
