@@ -285,7 +285,8 @@ def reference_planner():
         return None
 
 
-def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_mhz=None, sms=148, l2_peak=None):
+def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_mhz=None, sms=148, l2_peak=None,
+                   p_ffma_measured=None):
     """Roofline of the dominant kernel, the recurrence: t_roof = max(FLOPs /
     tensor peak, bytes / HBM bandwidth), so frac = max of the two fractions and
     `bound` names the larger.  FLOPs: the algorithmic recurrent FLOPs.  Bytes:
@@ -330,12 +331,14 @@ def roofline_entry(spec, plan, algo, rec_f, rec_ms, gemm_ms, peaks, traffic, sm_
         # clock measured under load (no byte term when W_hh is SMEM-resident).
         # The north-star target (recurrent kernel >= 50% of its roofline) is
         # stated against this; the kernel exceeds it because it runs on tcgen05.
-        p_ffma = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+        p_ffma = p_ffma_measured or sms * 128 * 2 * sm_mhz * 1e6 / 1e12
         wstream = (wbytes * slices if plan.get("w_ring") else 0.0) * T * spec.layers * spec.dirs
         t_roof = max(rec_f / (p_ffma * 1e12), wstream / (peaks["hbm_gbs"] * 1e9))
         out["survey_fp32_roofline"] = {"t_roof_ms": t_roof * 1e3, "kernel_ms": rec_ms, "frac": t_roof / sec,
                                        "p_ffma_tflops": p_ffma, "sm_mhz": sm_mhz, "sms": sms,
-                                       "note": "SURVEY 8d K2 formula (FP32 FFMA peak from the measured SM clock)"}
+                                       "note": "SURVEY 8d K2 formula; P_FFMA " + (
+                                           "measured (tools/peak_probe.py)" if p_ffma_measured else
+                                           "from the measured SM clock")}
     return out
 
 
@@ -602,12 +605,17 @@ def main(argv=None):
     plan = ex.plan()
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
+    l2_peak = p_ffma = None
     if tfile.exists():
         tdoc = json.loads(tfile.read_text())
         traffic = tdoc.get(f"{args.config}:{ex.algo}:recurrent")
         l2_peak = tdoc.get("_l2_peak")
-    else:
-        l2_peak = None
+    pfile = ROOT / "profiles" / "peaks_fp32_l2.json"  # tools/peak_probe.py on a B200 of this pool
+    if pfile.exists():
+        pdoc = json.loads(pfile.read_text())
+        l2_peak = {"gbs": pdoc["l2_read_gbs_64MiB"],
+                   "source": "measured L2 read of a 64 MiB L2-resident buffer (profiles/peaks_fp32_l2.json)"}
+        p_ffma = pdoc["ffma_tflops"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "p50_ms": p50, "p90_ms": p90,
@@ -621,7 +629,8 @@ def main(argv=None):
                    "e2e_l2": "no flush; per-request working set (2 x 128 MiB xproj + 32 MiB x + 32 MiB y) exceeds the 126 MB L2"},
         "roofline": roofline_entry(spec, plan, ex.algo, rec_f, rec_ms, gemm_ms, peaks, traffic,
                                    sm_mhz=clocks.summary().get("sm_mhz"),
-                                   sms=torch.cuda.get_device_properties(dev).multi_processor_count, l2_peak=l2_peak),
+                                   sms=torch.cuda.get_device_properties(dev).multi_processor_count, l2_peak=l2_peak,
+                                   p_ffma_measured=p_ffma),
         "plan": plan,
         "e2e": {"value": B_total * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
