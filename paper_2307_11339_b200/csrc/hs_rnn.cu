@@ -556,7 +556,7 @@ int gemm_stream(cudaStream_t* out) {
 }
 
 int copy_stream(int which, cudaStream_t* out) {
-  static thread_local cudaStream_t cache[2][16] = {};
+  static thread_local cudaStream_t cache[3][16] = {};
   int dev;
   HS_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return fail(HS_ERR_NO_DEVICE, "device index %d out of range", dev);
@@ -1312,20 +1312,33 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         CUresult r = wait(gs, reinterpret_cast<CUdeviceptr>(a.progress), ncta, 0 /*GEQ*/);
         if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
       }
-      const int nco = m.T < 16 ? m.T : 16;
+      static const char* nco_env = getenv("HS_DRAIN_CHUNKS");  // y drain chunks (A/B; default 16)
+      const int nco_req = nco_env && atoi(nco_env) > 0 ? atoi(nco_env) : 16;
+      const int nco = m.T < nco_req ? m.T : nco_req;
       const size_t row = (size_t)m.B * m.D * m.H;
+      // chunks alternate between two copy streams: a 2 MB D2H copy alone ran
+      // at ~39 GB/s with ~7 us gaps (c2 timeline); two in flight keep PCIe busy
+      cudaStream_t cs2 = nullptr;
+      static const char* two_env = getenv("HS_DRAIN_STREAMS");
+      const bool two_cs = wait && !(two_env && atoi(two_env) == 1);
+      if (two_cs) {
+        if ((rc = copy_stream(2, &cs2))) return rc;
+        if ((rc = join(ov->cs_out, cs2))) return rc;  // cs2 after everything cs_out was ordered behind
+      }
       for (int k = 0; k < nco; ++k) {
         int t0, t1;
         chunk_bounds(m.T, nco, k, &t0, &t1);
         const int s_need = m.D == 1 ? t1 - 1 : (t1 - 1 > m.T - 1 - t0 ? t1 - 1 : m.T - 1 - t0);
+        cudaStream_t cs = two_cs && (k & 1) ? cs2 : ov->cs_out;
         if (wait) {
-          CUresult r = wait(ov->cs_out, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
+          CUresult r = wait(cs, reinterpret_cast<CUdeviceptr>(a.progress + s_need), ncta, 0 /*GEQ*/);
           if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
         }
-        if (dbg && k < 8) HS_CUDA(cudaEventRecord(dbg_ev[2 + k], ov->cs_out));
+        if (dbg && k < 8) HS_CUDA(cudaEventRecord(dbg_ev[2 + k], cs));
         HS_CUDA(cudaMemcpyAsync(ov->y_host + (size_t)t0 * row, y + (size_t)t0 * row, (size_t)(t1 - t0) * row * sizeof(float),
-                                cudaMemcpyDeviceToHost, ov->cs_out));
+                                cudaMemcpyDeviceToHost, cs));
       }
+      if (two_cs && (rc = join(cs2, ov->cs_out))) return rc;  // the drain ends on cs_out
       if (dbg) {
         HS_CUDA(cudaEventRecord(dbg_ev[10], ov->cs_out));
         HS_CUDA(cudaEventSynchronize(dbg_ev[10]));
