@@ -214,6 +214,17 @@ typedef struct hs_stage_link {
   int32_t reserved[5];
 } hs_stage_link;
 
+/* Sharing a stage's link buffers with the neighbouring stage's process (the
+ * pipeline's setup step, SURVEY §8(b) "hs_pipeline_init"): export a device
+ * pointer as a 64-byte CUDA IPC handle plus its offset inside the allocation,
+ * import it in the other process (mapped once per allocation and process,
+ * reference-counted), release the mapping when the pipeline is torn down.
+ * Python callers can use torch.multiprocessing's CUDA sharing instead
+ * (parallel.PeerPipeline does). */
+int hs_pipeline_export(const void* dev_ptr, void* handle64, size_t* offset);
+int hs_pipeline_import(const void* handle64, size_t offset, void** dev_ptr);
+int hs_pipeline_release(void* dev_ptr);
+
 /* One pipeline stage's forward (tensor-core path, unidirectional): as
  * hs_rnn_forward_packed over this stage's layers, with the input taken from
  * link->x_planes chunk by chunk as x_avail advances (the first layer's input

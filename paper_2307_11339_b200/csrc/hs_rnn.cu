@@ -1734,6 +1734,75 @@ int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed, const void
   return HS_OK;
 }
 
+// ---- pipeline buffer sharing (CUDA IPC); one mapping per (device, allocation) per process
+namespace {
+struct IpcMap { char handle[64]; int dev; void* base; int refs; };
+std::mutex g_ipc_mu;
+IpcMap g_ipc[64];
+}  // namespace
+
+int hs_pipeline_export(const void* dev_ptr, void* handle64, size_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(HS_ERR_INVALID, "dev_ptr, handle64 and offset must be non-NULL");
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(HS_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<RangeFn>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(HS_ERR_INVALID, "pointer is not device memory of this process");
+  cudaIpcMemHandle_t h;
+  HS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle64, &h, 64);
+  *offset = (size_t)(reinterpret_cast<uintptr_t>(dev_ptr) - (uintptr_t)base);
+  return HS_OK;
+}
+
+int hs_pipeline_import(const void* handle64, size_t offset, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(HS_ERR_INVALID, "handle64 and dev_ptr must be non-NULL");
+  int dev = 0;
+  HS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (IpcMap& m : g_ipc)
+    if (m.refs > 0 && m.dev == dev && memcmp(m.handle, handle64, 64) == 0) {
+      ++m.refs;
+      *dev_ptr = static_cast<char*>(m.base) + offset;
+      return HS_OK;
+    }
+  for (IpcMap& m : g_ipc)
+    if (m.refs == 0) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handle64, 64);
+      void* base = nullptr;
+      HS_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      memcpy(m.handle, handle64, 64);
+      m.dev = dev;
+      m.base = base;
+      m.refs = 1;
+      *dev_ptr = static_cast<char*>(base) + offset;
+      return HS_OK;
+    }
+  return fail(HS_ERR_INVALID, "too many imported pipeline allocations (64)");
+}
+
+int hs_pipeline_release(void* dev_ptr) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  IpcMap* best = nullptr;  // the mapping with the highest base at or below the pointer
+  for (IpcMap& m : g_ipc)
+    if (m.refs > 0 && static_cast<char*>(dev_ptr) >= static_cast<char*>(m.base) && (!best || m.base > best->base))
+      best = &m;
+  if (!best) return fail(HS_ERR_INVALID, "pointer was not imported with hs_pipeline_import");
+  if (--best->refs == 0) HS_CUDA(cudaIpcCloseMemHandle(best->base));
+  return HS_OK;
+}
+
 int hs_rnn_forward_stage(const hs_rnn_desc* desc, const void* packed, const void* x, const void* h0, const void* c0,
                          void* y, void* hn, void* cn, const hs_stage_link* link, void* workspace, size_t ws_bytes,
                          void* stream) {

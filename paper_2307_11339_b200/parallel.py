@@ -294,6 +294,35 @@ def _open(shared):
     return fn(*args)
 
 
+def _hs_export(lib, t: torch.Tensor):
+    """(64-byte CUDA IPC handle, offset) of a device tensor (hs_pipeline_export)."""
+    import ctypes
+
+    from .rnn import _check
+
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_size_t()
+    _check(lib, "hs_pipeline_export", lib.hs_pipeline_export(t.data_ptr(), h, ctypes.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def _hs_import(lib, exported) -> int:
+    """Device address of a peer's exported tensor in this process (hs_pipeline_import)."""
+    import ctypes
+
+    from .rnn import _check
+
+    handle, off = exported
+    h = (ctypes.c_char * 64).from_buffer_copy(handle)
+    p = ctypes.c_void_p()
+    _check(lib, "hs_pipeline_import", lib.hs_pipeline_import(h, off, ctypes.byref(p)))
+    return int(p.value)
+
+
+def _addr(x) -> int:
+    return x if isinstance(x, int) else x.data_ptr()
+
+
 class PeerPipeline:
     """Stage ``rank`` of a layer pipeline with the stream-ordered peer hand-off.
 
@@ -309,7 +338,10 @@ class PeerPipeline:
     the IPC handles (any backend; gloo works for same-host ranks).
     """
 
-    def __init__(self, executor, rank: int, world: int, chunk: int = 32, group=None):
+    def __init__(self, executor, rank: int, world: int, chunk: int = 32, group=None, share: str = "torch"):
+        """``share``: how the link buffers cross processes — "torch"
+        (torch.multiprocessing's CUDA tensor sharing) or "hs" (the library's
+        own ``hs_pipeline_export`` / ``hs_pipeline_import`` C ABI)."""
         from .rnn import StageLink
 
         self.ex, self.rank, self.world = executor, rank, world
@@ -326,21 +358,25 @@ class PeerPipeline:
             self.x_avail = torch.zeros(1, dtype=torch.int32, device=dev)
         if rank < world - 1:
             self.consumed = torch.zeros(1, dtype=torch.int32, device=dev)
-        mine = {"slots": _share(self.slots) if self.slots is not None else None,
-                "x_avail": _share(self.x_avail) if self.x_avail is not None else None,
-                "consumed": _share(self.consumed) if self.consumed is not None else None}
+        if share not in ("torch", "hs"):
+            raise ValueError(f"unknown share mode {share!r}")
+        self.share = share
+        exp = _share if share == "torch" else (lambda t: _hs_export(executor.lib, t))
+        mine = {k: exp(t) if t is not None else None
+                for k, t in (("slots", self.slots), ("x_avail", self.x_avail), ("consumed", self.consumed))}
         torch.cuda.synchronize(dev)
         allv = [mine]
         if world > 1:
             allv = [None] * world
             dist.all_gather_object(allv, mine, group=group)
+        imp = _open if share == "torch" else (lambda h: _hs_import(executor.lib, h))
         self.next_slots = self.next_avail = self.prev_consumed = None
         if rank < world - 1:
             nxt = allv[rank + 1]
-            self.next_slots = _open(nxt["slots"])
-            self.next_avail = _open(nxt["x_avail"])
+            self.next_slots = imp(nxt["slots"])
+            self.next_avail = imp(nxt["x_avail"])
         if rank > 0:
-            self.prev_consumed = _open(allv[rank - 1]["consumed"])
+            self.prev_consumed = imp(allv[rank - 1]["consumed"])
         self._keep = allv
         self.seq = 0  # global request counter (the monotonic counters' base)
 
@@ -352,11 +388,14 @@ class PeerPipeline:
             lk.x_planes = self.slots[v["slot"]].data_ptr()
             lk.x_avail = self.x_avail.data_ptr()
             lk.x_base = v["x_base"]
-            lk.consumed_peer = self.prev_consumed.data_ptr()
+            lk.consumed_peer = _addr(self.prev_consumed)
             lk.consumed_value = v["consumed_value"]
         if self.rank < self.world - 1:
-            lk.y_peer_planes = self.next_slots[v["slot"]].data_ptr()
-            lk.y_peer_avail = self.next_avail.data_ptr()
+            if self.share == "hs":  # a raw address: slots of the next stage are [2][2][T*B][H] bf16
+                lk.y_peer_planes = self.next_slots + v["slot"] * (2 * self.T * self.B * self.ex.spec.hidden * 2)
+            else:
+                lk.y_peer_planes = self.next_slots[v["slot"]].data_ptr()
+            lk.y_peer_avail = _addr(self.next_avail)
             lk.y_base = v["y_base"]
             lk.consumed = self.consumed.data_ptr()
             lk.consumed_wait = v["consumed_wait"]

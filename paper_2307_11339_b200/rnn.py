@@ -53,6 +53,9 @@ ABI_SYMBOLS = (
     "hs_rnn_forward",
     "hs_rnn_forward_host",
     "hs_rnn_forward_stage",
+    "hs_pipeline_export",
+    "hs_pipeline_import",
+    "hs_pipeline_release",
     "hs_rnn_outputs_ready",
     "hs_rnn_run_cells",
 )
@@ -206,6 +209,9 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     lib.hs_rnn_forward_host.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.hs_rnn_forward_stage.argtypes = [pd, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(StageLink), vp, sz, vp]
     lib.hs_rnn_outputs_ready.argtypes = [vp, vp]
+    lib.hs_pipeline_export.argtypes = [vp, vp, ctypes.POINTER(sz)]
+    lib.hs_pipeline_import.argtypes = [vp, sz, ctypes.POINTER(vp)]
+    lib.hs_pipeline_release.argtypes = [vp]
     lib.hs_rnn_run_cells.argtypes = [pd, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ABI_SYMBOLS[3:]:
         getattr(lib, name).restype = ctypes.c_int

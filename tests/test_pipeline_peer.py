@@ -125,7 +125,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, spec, chunk, nreq, q):
+def _ipc_worker(rank, world, port, spec, chunk, nreq, q, share="torch"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -136,7 +136,7 @@ def _ipc_worker(rank, world, port, spec, chunk, nreq, q):
         w = init_weights(spec, 9)
         l0, l1 = stage_layers(spec.layers, world, rank)
         sspec = spec.with_(layers=l1 - l0, input=spec.I if rank == 0 else spec.hidden)
-        pipe = PeerPipeline(RNNExecutor(sspec, w[l0:l1]), rank, world, chunk=chunk)
+        pipe = PeerPipeline(RNNExecutor(sspec, w[l0:l1]), rank, world, chunk=chunk, share=share)
         xs = [make_input(spec, 30 + r) for r in range(nreq)]
         res = pipe.run_many(xs if rank == 0 else [None] * nreq)
         torch.cuda.synchronize()
@@ -154,13 +154,15 @@ def _ipc_worker(rank, world, port, spec, chunk, nreq, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_pipeline_two_processes_cuda_ipc(world):
+@pytest.mark.parametrize("world,share", [(2, "torch"), (3, "torch"), (3, "hs")])
+def test_peer_pipeline_two_processes_cuda_ipc(world, share):
+    """share="hs": the buffers cross processes through the library's own
+    hs_pipeline_export / hs_pipeline_import C ABI instead of torch's."""
     spec = RNNSpec("lstm", 3, 256, 16, 16, algo="tc")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, spec, 4, 3, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, spec, 4, 3, q, share)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=300) for _ in procs)
