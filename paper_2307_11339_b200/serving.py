@@ -319,70 +319,83 @@ class Scenario:
 
 
 _MODEL_KEYS = ("id", "gpu_footprint_mb", "exec_latency_ms", "weights_mb", "slo_ms")
+_WORKLOAD_DEFAULTS = (("pattern", str, "uniform"), ("seed", int, 0), ("interarrival_ms", float, 0.0))
 
 
-def _entry_doc(m: ModelEntry) -> dict:
-    return {k: getattr(m, k) for k in _MODEL_KEYS}
+def _bad(where: str, what: str):
+    return ScenarioError(f"{where}: {what}")
 
 
-def _entry(doc, where: str) -> ModelEntry:
+def _model(doc, where: str) -> ModelEntry:
+    """One model entry of a scenario file (the five _MODEL_KEYS; numbers >= 0)."""
     if not isinstance(doc, dict):
-        raise ScenarioError(f"{where}: model entries must be objects")
-    for k in _MODEL_KEYS:
-        if k not in doc:
-            raise ScenarioError(f"{where}: model entry missing key {k!r}")
+        raise _bad(where, "model entries must be objects")
+    absent = [k for k in _MODEL_KEYS if k not in doc]
+    if absent:
+        raise _bad(where, f"model entry missing key {absent[0]!r}")
     if not isinstance(doc["id"], str):
-        raise ScenarioError(f"{where}: model id must be a string")
+        raise _bad(where, "model id must be a string")
+    nums = []
     for k in _MODEL_KEYS[1:]:
-        if not isinstance(doc[k], (int, float)) or doc[k] < 0:
-            raise ScenarioError(f"{where}: {k} must be a non-negative number")
-    return ModelEntry(doc["id"], *(float(doc[k]) for k in _MODEL_KEYS[1:]))
+        v = doc[k]
+        if isinstance(v, bool) or not isinstance(v, (int, float)) or v < 0:
+            raise _bad(where, f"{k} must be a non-negative number")
+        nums.append(float(v))
+    return ModelEntry(doc["id"], *nums)
+
+
+def _model_list(lst, where: str) -> tuple[ModelEntry, ...]:
+    if not isinstance(lst, list) or not lst:
+        raise _bad(where, "expected a non-empty list of models")
+    return tuple(_model(m, f"{where}[{i}]") for i, m in enumerate(lst))
 
 
 def save_scenario(scenario: Scenario, path) -> None:
+    """Write a scenario file (the reference's format, servingsim.py:353-376)."""
     w = scenario.workload
-    doc: dict = {"capacity_mb": scenario.capacity_mb, "bandwidth_mb_per_ms": scenario.bandwidth_mb_per_ms,
-                 "workload": {"total_requests": w.total_requests, "pattern": w.pattern, "seed": w.seed,
-                              "interarrival_ms": w.interarrival_ms}}
-    if scenario.models is not None:
-        doc["models"] = [_entry_doc(m) for m in scenario.models]
+    rows = lambda ms: [{k: getattr(m, k) for k in _MODEL_KEYS} for m in ms]  # noqa: E731
+    doc: dict = {
+        "capacity_mb": scenario.capacity_mb,
+        "bandwidth_mb_per_ms": scenario.bandwidth_mb_per_ms,
+        "workload": dict(total_requests=w.total_requests, **{k: getattr(w, k) for k, _, _ in _WORKLOAD_DEFAULTS}),
+    }
+    if scenario.models is None:
+        doc["patterns"] = {name: rows(ms) for name, ms in scenario.patterns.items()}
     else:
-        doc["patterns"] = {k: [_entry_doc(m) for m in v] for k, v in scenario.patterns.items()}
+        doc["models"] = rows(scenario.models)
     Path(path).write_text(json.dumps(doc, indent=2) + "\n")
 
 
 def load_scenario(path) -> Scenario:
+    """Read a scenario file; any inconsistency raises ScenarioError
+    (servingsim.py:379-427)."""
     try:
         doc = json.loads(Path(path).read_text())
     except json.JSONDecodeError as exc:
-        raise ScenarioError(f"{path}: not valid JSON: {exc}") from exc
+        raise _bad(str(path), f"not valid JSON: {exc}") from exc
     if not isinstance(doc, dict):
-        raise ScenarioError(f"{path}: expected a JSON object")
+        raise _bad(str(path), "expected a JSON object")
     for k in ("capacity_mb", "bandwidth_mb_per_ms", "workload"):
         if k not in doc:
-            raise ScenarioError(f"{path}: missing key {k!r}")
+            raise _bad(str(path), f"missing key {k!r}")
     wd = doc["workload"]
     if not isinstance(wd, dict) or "total_requests" not in wd:
-        raise ScenarioError(f"{path}: workload must be an object with total_requests")
-    workload = Workload(int(wd["total_requests"]), str(wd.get("pattern", "uniform")), int(wd.get("seed", 0)),
-                        float(wd.get("interarrival_ms", 0.0)))
+        raise _bad(str(path), "workload must be an object with total_requests")
+    extra = {k: cast(wd.get(k, dflt)) for k, cast, dflt in _WORKLOAD_DEFAULTS}
+    workload = Workload(total_requests=int(wd["total_requests"]), **extra)
     if workload.pattern not in ("uniform", "random"):
-        raise ScenarioError(f"{path}: unknown workload pattern {workload.pattern!r}")
-    if ("models" in doc) == ("patterns" in doc):
-        raise ScenarioError(f"{path}: need exactly one of 'models' or 'patterns'")
+        raise _bad(str(path), f"unknown workload pattern {workload.pattern!r}")
+    has = [k for k in ("models", "patterns") if k in doc]
+    if len(has) != 1:
+        raise _bad(str(path), "need exactly one of 'models' or 'patterns'")
     models = patterns = None
-    if "models" in doc:
-        if not isinstance(doc["models"], list) or not doc["models"]:
-            raise ScenarioError(f"{path}: models must be a non-empty list")
-        models = tuple(_entry(m, f"{path} models[{i}]") for i, m in enumerate(doc["models"]))
+    if has[0] == "models":
+        models = _model_list(doc["models"], f"{path} models")
     else:
-        if not isinstance(doc["patterns"], dict) or not doc["patterns"]:
-            raise ScenarioError(f"{path}: patterns must be a non-empty object")
-        patterns = {}
-        for name, lst in doc["patterns"].items():
-            if not isinstance(lst, list) or not lst:
-                raise ScenarioError(f"{path}: pattern {name!r} must hold a non-empty model list")
-            patterns[name] = tuple(_entry(m, f"{path} patterns[{name}][{i}]") for i, m in enumerate(lst))
+        pd = doc["patterns"]
+        if not isinstance(pd, dict) or not pd:
+            raise _bad(str(path), "patterns must be a non-empty object")
+        patterns = {name: _model_list(lst, f"{path} patterns[{name}]") for name, lst in pd.items()}
     return Scenario(float(doc["capacity_mb"]), float(doc["bandwidth_mb_per_ms"]), workload, models, patterns)
 
 
