@@ -1688,7 +1688,11 @@ int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed, const void
                     static_cast<const float*>(c0), static_cast<float*>(y), static_cast<float*>(hn),
                     static_cast<float*>(cn), workspace, wl, s, nullptr);
   g_stamps = nullptr;
-  if (rc) return rc;
+  if (rc) {
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return rc;
+  }
   HS_CUDA(cudaEventRecord(ev[1], s));
   std::vector<unsigned long long> h(nst);
   HS_CUDA(cudaMemcpyAsync(h.data(), st, nst * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1736,23 +1740,27 @@ int hs_rnn_profile_cells(const hs_rnn_desc* desc, const void* packed, const void
 
 // ---- pipeline buffer sharing (CUDA IPC); one mapping per (device, allocation) per process
 namespace {
-struct IpcMap { char handle[64]; int dev; void* base; int refs; };
+struct IpcMap { char handle[64]; int dev; void* base; size_t size; int refs; };
+typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+RangeFn address_range_fn() {
+  static RangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<RangeFn>(p);
+  }
+  return fn;
+}
 std::mutex g_ipc_mu;
 IpcMap g_ipc[64];
 }  // namespace
 
 int hs_pipeline_export(const void* dev_ptr, void* handle64, size_t* offset) {
   if (!dev_ptr || !handle64 || !offset) return fail(HS_ERR_INVALID, "dev_ptr, handle64 and offset must be non-NULL");
-  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static RangeFn range = nullptr;
-  if (!range) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return fail(HS_ERR_CUDA, "cuMemGetAddressRange unavailable");
-    range = reinterpret_cast<RangeFn>(p);
-  }
+  RangeFn range = address_range_fn();
+  if (!range) return fail(HS_ERR_CUDA, "cuMemGetAddressRange unavailable");
   CUdeviceptr base = 0;
   size_t size = 0;
   if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
@@ -1782,9 +1790,14 @@ int hs_pipeline_import(const void* handle64, size_t offset, void** dev_ptr) {
       memcpy(&h, handle64, 64);
       void* base = nullptr;
       HS_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      CUdeviceptr b0 = 0;
+      size_t size = 0;
+      RangeFn range = address_range_fn();
+      if (range) range(&b0, &size, reinterpret_cast<CUdeviceptr>(base));
       memcpy(m.handle, handle64, 64);
       m.dev = dev;
       m.base = base;
+      m.size = size;
       m.refs = 1;
       *dev_ptr = static_cast<char*>(base) + offset;
       return HS_OK;
@@ -1794,9 +1807,11 @@ int hs_pipeline_import(const void* handle64, size_t offset, void** dev_ptr) {
 
 int hs_pipeline_release(void* dev_ptr) {
   std::lock_guard<std::mutex> lk(g_ipc_mu);
-  IpcMap* best = nullptr;  // the mapping with the highest base at or below the pointer
+  IpcMap* best = nullptr;  // the mapping that contains the pointer
   for (IpcMap& m : g_ipc)
-    if (m.refs > 0 && static_cast<char*>(dev_ptr) >= static_cast<char*>(m.base) && (!best || m.base > best->base))
+    if (m.refs > 0 && static_cast<char*>(dev_ptr) >= static_cast<char*>(m.base) &&
+        (m.size == 0 || static_cast<char*>(dev_ptr) < static_cast<char*>(m.base) + m.size) &&
+        (!best || m.base > best->base))
       best = &m;
   if (!best) return fail(HS_ERR_INVALID, "pointer was not imported with hs_pipeline_import");
   if (--best->refs == 0) HS_CUDA(cudaIpcCloseMemHandle(best->base));
