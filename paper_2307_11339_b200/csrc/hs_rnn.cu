@@ -1096,7 +1096,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     // enough for both chains to carry work: c2 (B=64) 6.85 -> 6.58 us/step;
     // slower at B=32 (c3: 4.25 -> 4.68 ms).  HS_TWO_GROUPS=0/1 overrides.
     static const char* two_env = getenv("HS_TWO_GROUPS");
-    const bool two_req = two_env ? atoi(two_env) == 1 : m.B >= 64;
+    // (bidirectional: from 32 rows — c5's 8-way shard, B=32: 1,124 -> 1,174 seqs/s)
+    const bool two_req = two_env ? atoi(two_env) == 1 : (m.B >= 64 || (m.D == 2 && m.B >= 32));
     const bool two = nsl == 1 && two_req && choose_split2(m.G, m.H, m.B, m.D, NPL) > 0;
     // ---- XP streaming of this layer's K1 (head on s now, side part after the launch)
     const int tiles_m = (int)((TB + 127) / 128), per_m = m.D * (m.G * m.H / 256), tiles_all = tiles_m * per_m;
@@ -1221,7 +1222,8 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         }
         // a slice of >= 64 sequences runs as two batch-half chains too (W_hh in
         // TMEM where the shared-memory layout does not fit, e.g. c5's slices)
-        const bool two_slice = (two_env ? atoi(two_env) == 1 : bn >= 64) && choose_split2(m.G, m.H, bn, m.D, NPL) > 0;
+        const bool two_slice = (two_env ? atoi(two_env) == 1 : (bn >= 64 || (m.D == 2 && bn >= 32))) &&
+                               choose_split2(m.G, m.H, bn, m.D, NPL) > 0;
         rc = two_slice ? recurrence_layer2(m.G, NPL, whh, sa, s, g_err)
                        : recurrence_layer(m.G, NPL, whh, sa, di.sms, s, g_err);
         if (rc) return rc;
