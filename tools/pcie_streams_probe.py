@@ -24,7 +24,7 @@ for direction in ("d2h", "h2d"):
                     else:
                         src[i * part:(i + 1) * part].copy_(hsrc[i * part:(i + 1) * part], non_blocking=True)
             for s in streams:
-                e1.wait(s) if False else torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.current_stream().wait_stream(s)
             e1.record()
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
