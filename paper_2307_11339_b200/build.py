@@ -53,15 +53,17 @@ def needs_build() -> bool:
     return any(src.stat().st_mtime > t for src in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines: tuple = ()) -> Path:
     """Compile ``csrc/hs_rnn.cu`` (which includes every kernel header) into
-    ``_lib/libhsrnn.so``.  Returns the library path."""
-    lib = library_path()
+    ``_lib/libhsrnn.so`` (or ``out``, with extra ``-D`` defines: variant builds
+    for experiments, loaded through ``HS_LIB_PATH``).  Returns the library path."""
+    lib = Path(out) if out else library_path()
     if not force and not needs_build():
         return lib
     LIBDIR.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), str(CSRC / "hs_rnn.cu")]
+    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", str(INCLUDE), "-o", str(tmp),
+           str(CSRC / "hs_rnn.cu")]
     if verbose:
         cmd += ["-Xptxas", "-v"]
         print(" ".join(cmd))

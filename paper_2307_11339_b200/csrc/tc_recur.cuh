@@ -164,11 +164,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define HS_TRACE(phase)                                                                          \
+#define HS_TRACE_AT(phase)                                                                       \
   do {                                                                                           \
     if (a.trace && s < kTraceSteps && blockIdx.x < kTraceCtas)                                   \
       a.trace[((size_t)blockIdx.x * kTraceSteps + s) * 16 + (phase)] = globaltimer();             \
   } while (0)
+// HS_TRACE_CHUNKS (diagnostic variant build, tools/trace_chunks.py): the MMA
+// issuer first waits for every h chunk of the step in order, recording when
+// each landed (slots 0..13), then times the W-streaming variant's TMEM-chunk
+// MMAs alone into a scratch accumulator (slot 14); no phase stamps
+#ifdef HS_TRACE_CHUNKS
+#define HS_TRACE(phase) do { } while (0)
+#else
+#define HS_TRACE(phase) HS_TRACE_AT(phase)
+#endif
 
 constexpr int kMaxSW = 8;  // W-streaming ring depth limit
 
@@ -302,6 +311,9 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       ptx::mbar_init(&wfull[i], 1);
       ptx::mbar_init(&wempty[i], 1);
     }
+#ifdef HS_TRACE_CHUNKS
+    if (NSW < kMaxSW) ptx::mbar_init(&wfull[kMaxSW - 1], 1);
+#endif
     ptx::mbar_init(red_full, 9);
     ptx::mbar_init(red_free, (uint32_t)(S * 8));
     ptx::mbar_init(tmem_free, 8);
@@ -463,6 +475,31 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
       if (ptx::elect_one()) {
         if (NSW == 0 && s == 0 && !wt) ptx::mbar_wait(w_full, 0);
         if (s > 0) ptx::mbar_wait(tmem_free, (s - 1) & 1);  // every warp drained step s-1
+#ifdef HS_TRACE_CHUNKS
+        for (int c = 0; c < nch; ++c) {
+          ptx::mbar_wait(&h_full[c], s & 1);
+          if (c < 14) HS_TRACE_AT(c);
+        }
+        if (nres && tcols_acc + (uint32_t)(nres * NPL * 32) + 32u <= 512u) {
+          // the TMEM chunks' MMAs once more into a scratch accumulator (the
+          // free columns after the resident W), back to back
+          const uint32_t scratch = tmem + tcols_acc + (uint32_t)(nres * NPL * 32);
+          ptx::tc_fence_after();
+          for (int c = 0; c < nres; ++c) {
+            const __nv_bfloat16* hh = sH + (size_t)c * Npad * 64;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = ptx::sdesc_k_sw128(hh + kk * 16);
+              const uint32_t wc = tmem + tcols_acc + (uint32_t)(c * NPL * 32 + kk * 8);
+              ptx::mma_bf16_ts(scratch, wc, bd, idesc, (c | kk) != 0);
+              if (NPL == 2) ptx::mma_bf16_ts(scratch, wc + 32u, bd, idesc, 1);
+            }
+          }
+          ptx::mma_commit(&wfull[kMaxSW - 1]);
+          ptx::mbar_wait(&wfull[kMaxSW - 1], s & 1);
+          HS_TRACE_AT(14);
+        }
+#endif
         for (int c = 0; c < nch; ++c) {
           const bool in_tmem = c < nres;  // W-streaming variant: resident chunk, no ring slot
           const int gi = s * nstream + (c - nres), wslot = NSW && !in_tmem ? gi % NSW : 0;

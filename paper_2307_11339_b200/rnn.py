@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, replace
 from pathlib import Path
 
@@ -181,7 +182,8 @@ def load_library(path: str | Path | None = None, build_if_missing: bool = False)
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    lib_path = Path(path) if path else _build.library_path()
+    # HS_LIB_PATH: a variant build of the same sources (A/B experiments, debug traces)
+    lib_path = Path(path) if path else Path(os.environ.get("HS_LIB_PATH") or _build.library_path())
     if not lib_path.exists():
         if build_if_missing:
             lib_path = _build.build()
