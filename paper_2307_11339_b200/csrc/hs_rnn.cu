@@ -862,7 +862,18 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
   const int Bs = batch_slice(m.G, m.H, m.B, m.D, NPL);
   if (!Bs) return fail(HS_ERR_UNSUPPORTED, "no tensor-core recurrence plan for B=%d", m.B);
   const int nsl = (m.B + Bs - 1) / Bs;
-  const bool overlap = nsl == 1 && m.L > 1 && wait_value_fn() != nullptr && !(ovl_env && strcmp(ovl_env, "0") == 0);
+  // CUDA-graph capture (RNNExecutor.graph): one stream, one chain of launches.
+  // The overlapped schedules run kernels on a second stream that spin on each
+  // other's progress counters; a graph may launch sibling nodes in either
+  // order, so a captured forward runs the layers back to back instead (same
+  // tiles, same accumulation order: bit-identical results).
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HS_CUDA(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (capturing && (ov || layer_ms))
+    return fail(HS_ERR_UNSUPPORTED, "only device-buffer forwards without layer timing can be captured into a CUDA graph");
+  const bool overlap = !capturing && nsl == 1 && m.L > 1 && wait_value_fn() != nullptr &&
+                       !(ovl_env && strcmp(ovl_env, "0") == 0);
   // single-GPU layer wavefront (tc_wave.cuh): all layers in one cooperative launch
   // the static plan, re-checked against the device's occupancy (a co-tenant,
   // MIG slice or cluster placement may fit fewer CTAs): two CTAs per SM, then one

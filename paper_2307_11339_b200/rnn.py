@@ -262,6 +262,26 @@ def _ptr_array(ts):
     return arr
 
 
+class GraphedForward:
+    """One captured device forward (``RNNExecutor.graph``): ``x`` is the static
+    input buffer, ``y`` / ``h_n`` / ``c_n`` the outputs every replay writes."""
+
+    def __init__(self, g, x, out):
+        self.g = g
+        self.x = x
+        self.y, self.h_n, self.c_n = out
+
+    def replay(self, x: torch.Tensor | None = None):
+        """Copy ``x`` (if given) into the static input on the current stream,
+        replay the graph, return ``(y, h_n, c_n)`` (the static outputs)."""
+        if x is not None:
+            if tuple(x.shape) != tuple(self.x.shape):
+                raise ValueError(f"x has shape {tuple(x.shape)}, expected {tuple(self.x.shape)}")
+            self.x.copy_(x)
+        self.g.replay()
+        return self.y, self.h_n, self.c_n
+
+
 class RNNExecutor:
     """A (bi)directional LSTM/GRU resident on one B200.
 
@@ -425,6 +445,37 @@ class RNNExecutor:
         if layer_ms:
             return y, hn, cn, [[times[2 * l], times[2 * l + 1]] for l in range(s.layers)]
         return y, hn, cn
+
+    def graph(self, h0=None, c0=None, warmup: int = 2) -> "GraphedForward":
+        """Capture one device forward into a CUDA graph (``torch.cuda.CUDAGraph``).
+
+        Launch-bound shapes (small layers, short sequences: the per-request
+        models of a serving loop) pay their launch and host costs once at
+        capture; ``GraphedForward.replay`` then re-runs every kernel of the
+        forward with one graph launch.  The captured forward runs its layers
+        back to back on one stream: the overlapped schedules (next-layer K1 and
+        XP streaming on a second stream, which spin on each other's progress
+        counters) are off, since a graph may start sibling nodes in either
+        order.  The results are bit-identical to ``forward`` (same tiles, same
+        accumulation order).  ``h0`` / ``c0`` are captured by address."""
+        self._require_resident()
+        s = self.spec
+        state = (s.layers * s.dirs, s.batch, s.hidden)
+        self._check_dev("h0", h0, state)
+        self._check_dev("c0", c0 if s.cell == "lstm" else None, state)
+        x = torch.zeros((s.seq, s.batch, s.I), device=self.device)
+        out = self.alloc_outputs()
+        with torch.cuda.device(self.device):
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):  # plans, lazy module loads, one-time probes: before the capture
+                for _ in range(max(1, warmup)):
+                    self.forward(x, h0, c0, out=out)
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.forward(x, h0, c0, out=out)
+        return GraphedForward(g, x, out)
 
     def profile_cells(self, x: torch.Tensor, h0=None, c0=None, out=None):
         """Per-cell GPU cost (ms) of the whole-DAG forward, ``hs_rnn_profile_cells``:
