@@ -23,7 +23,11 @@ namespace hs {
 constexpr int kSmallThreads = 256;
 
 struct SmallArgs {
-  int H, I, B, T, D, C;          // C = cluster size (CTAs per direction)
+  int H, I, B, T, D, C;          // C = cluster size (CTAs per direction); D = directions launched
+  // directions dir0 .. dir0+D-1 of a Dy-direction layer, steps s_base .. s_base+T-1
+  // of T_full (one plan segment, hs_rnn_run_cells); the fused forward runs
+  // dir0 = 0, Dy = D, s_base = 0, T_full = T
+  int dir0, Dy, s_base, T_full;
   const float* x;                // layer input [T][B][I]
   const float* w_ih[2];          // per dir [G*H][I] fp32 (PyTorch layout)
   const float* w_hh[2];          // per dir [G*H][H] fp32
@@ -31,7 +35,7 @@ struct SmallArgs {
   const float* bias_h[2];        // per dir [G*H] (GRU b_hh) or nullptr
   const float* h0[2];            // per dir [B][H], nullptr = zeros
   const float* c0[2];            // nullptr = zeros
-  float* y;                      // [T][B][D*H]
+  float* y;                      // [T_full][B][Dy*H]
   float* hn[2];                  // per dir [B][H]
   float* cn[2];
 };
@@ -82,10 +86,11 @@ __device__ __forceinline__ void small_matvec(const float* __restrict__ w, const 
 template <int G>
 __global__ void __launch_bounds__(kSmallThreads, 1) recur_cluster_small(const SmallArgs a) {
   extern __shared__ __align__(16) float sm[];
-  const int H = a.H, I = a.I, B = a.B, T = a.T, D = a.D, C = a.C;
+  const int H = a.H, I = a.I, B = a.B, T = a.T, C = a.C;
   const int U = H / C, rows = G * U;
   const int q = (int)ptx::cluster_rank();
-  const int d = blockIdx.x / C;
+  const int d = a.dir0 + (int)blockIdx.x / C;
+  const int Tf = a.T_full, sb = a.s_base, Dy = a.Dy;
   float* w_ih = sm;                                  // [rows][I]
   float* w_hh = w_ih + (size_t)rows * I;             // [rows][H]
   float* hbuf = w_hh + (size_t)rows * H;             // [2][B][H]
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) recur_cluster_small(const Sm
   while (tpi_h < 32 && rows * B * tpi_h * 2 <= kSmallThreads && tpi_h * 2 <= H / 4) tpi_h *= 2;
   __syncthreads();
   auto x_term = [&](int step, float* out) {
-    const int tt = d == 0 ? step : T - 1 - step;
+    const int tt = d == 0 ? sb + step : Tf - 1 - sb - step;
     small_matvec(w_ih, a.x + (size_t)tt * B * I, rows, B, I, I, out, B, tpi_x, bx);
   };
   x_term(0, xpart);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) recur_cluster_small(const Sm
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
   for (int s = 0; s < T; ++s) {
-    const int t = d == 0 ? s : T - 1 - s;
+    const int t = d == 0 ? sb + s : Tf - 1 - sb - s;
     const float* hcur = hbuf + (size_t)(s & 1) * B * H;
     float* hnext_local = hbuf + (size_t)((s + 1) & 1) * B * H;
     const float* xp = xpart + (size_t)(s & 1) * rows * B;
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) recur_cluster_small(const Sm
     for (int i = tid; i < U * B; i += kSmallThreads) {
       const int u = i / B, b = i % B;
       const int unit = q * U + u;
-      a.y[((size_t)t * B + b) * D * H + (size_t)d * H + unit] = ystage[i];
+      a.y[((size_t)t * B + b) * Dy * H + (size_t)d * H + unit] = ystage[i];
       if (s == T - 1) {
         a.hn[d][(size_t)b * H + unit] = ystage[i];
         if (G == 4) a.cn[d][(size_t)b * H + unit] = cst[i];

@@ -319,7 +319,7 @@ int launch_gemm_simt(const float* A, const float* Bw, const float* bias, float* 
 int launch_small(const Dims& m, const hs::SmallArgs& sa, cudaStream_t s) {
   const size_t smem = hs::small_smem_bytes(m.G, m.H, sa.I, m.B, sa.C);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(m.D * sa.C);
+  cfg.gridDim = dim3(sa.D * sa.C);
   cfg.blockDim = dim3(hs::kSmallThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -1415,6 +1415,7 @@ int forward_impl(const Dims& m, int algo, const DeviceInfo& di, const PackLayout
     if (C) {  // whole layer in one cluster per direction (input projection fused)
       hs::SmallArgs sa{};
       sa.H = m.H; sa.I = Il; sa.B = m.B; sa.T = m.T; sa.D = m.D; sa.C = C;
+      sa.dir0 = 0; sa.Dy = m.D; sa.s_base = 0; sa.T_full = m.T;
       sa.x = in;
       sa.y = out;
       for (int d = 0; d < m.D; ++d) {
@@ -2001,6 +2002,25 @@ int hs_rnn_run_cells(const hs_rnn_desc* desc, const void* packed, int32_t ld, in
   }
   const int l = ld / m.D, d = ld % m.D;
   const LayerPack& lp = pl.ld[ld];
+  const int C = lp.whh ? small_cluster(m) : 0;
+  if (algo != HS_ALGO_TC && C && !(seg_env && atoi(seg_env) == 1)) {
+    // the fused forward's small-shape kernel over this segment only (one
+    // cluster, input projection fused): what profile_ops measured for this shape
+    hs::SmallArgs sa{};
+    sa.H = m.H; sa.I = m.in_size(l); sa.B = m.B; sa.T = t1 - t0; sa.D = 1; sa.C = C;
+    sa.dir0 = d; sa.Dy = m.D; sa.s_base = t0; sa.T_full = m.T;
+    sa.x = static_cast<const float*>(in);
+    sa.y = static_cast<float*>(out);
+    sa.w_ih[d] = at<float>(packed, lp.wih);
+    sa.w_hh[d] = at<float>(packed, lp.whh);
+    sa.bias_x[d] = at<float>(packed, lp.bias_x);
+    sa.bias_h[d] = m.G == 3 ? at<float>(packed, lp.bias_h) : nullptr;
+    sa.h0[d] = static_cast<const float*>(h_prev);
+    sa.c0[d] = m.G == 4 ? static_cast<const float*>(c_prev) : nullptr;
+    sa.hn[d] = static_cast<float*>(h_last);
+    sa.cn[d] = m.G == 4 ? static_cast<float*>(c_last) : at<float>(workspace, wl.cst);
+    return launch_small(m, sa, s);
+  }
   // Input projection for the processed timesteps only: rows [tlo, thi) of `in`.
   const int tlo = d == 0 ? t0 : m.T - t1, thi = d == 0 ? t1 : m.T - t0;
   float* xp = at<float>(workspace, wl.xproj) + (size_t)d * m.T * m.B * m.G * m.H;

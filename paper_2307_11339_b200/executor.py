@@ -221,10 +221,17 @@ def build_schedule(graph: Graph, plan, spec) -> Schedule:
 
 @dataclass
 class ExecResult:
+    """Outputs of one plan execution.  ``trace.makespan`` follows the
+    reference's definition (engine.py:408-415): the last node's end, or a
+    host-bound transfer's; ``wall_ms`` is the whole call as the caller sees
+    it, including the final assembly of host-produced rows into ``y`` /
+    ``h_n`` / ``c_n`` on the device."""
+
     y: torch.Tensor
     hn: torch.Tensor
     cn: torch.Tensor | None
     trace: Trace
+    wall_ms: float = 0.0
 
 
 # ------------------------------------------------------------------ execute
@@ -257,7 +264,10 @@ def _execute_fused(graph, sched, ex, x, h0, c0) -> ExecResult:
     x = x.to(dev, torch.float32).contiguous()
     h0 = h0.to(dev, torch.float32).contiguous() if h0 is not None else None
     c0 = c0.to(dev, torch.float32).contiguous() if c0 is not None else None
+    t0 = time.perf_counter()
     y, hn, cn, lm = ex.forward(x, h0, c0, layer_ms=True)
+    torch.cuda.synchronize(dev)
+    wall = (time.perf_counter() - t0) * 1e3
     T, D = spec.seq, spec.dirs
     spans = []
     off = 0.0
@@ -270,7 +280,7 @@ def _execute_fused(graph, sched, ex, x, h0, c0) -> ExecResult:
                 spans.append(NodeSpan(v, GPU, off + s * dt, off + (s + 1) * dt))
         off += g_ms + r_ms
     spans.sort(key=lambda sp: (sp.start, sp.node))
-    return ExecResult(y, hn, cn, Trace(nodes=tuple(spans), transfers=(), makespan=off))
+    return ExecResult(y, hn, cn, Trace(nodes=tuple(spans), transfers=(), makespan=off), wall_ms=wall)
 
 
 class _Failure:
@@ -361,9 +371,16 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
             h0_d = h0_h.to(dev)
             c0_d = c0_h.to(dev) if lstm else None
             ev0 = torch.cuda.Event(enable_timing=True)
+            # every timing event of the run, created (and its CUDA event
+            # materialised) before the clock starts: per segment 2, per
+            # crossing 2
+            n_ev = 2 * len(sched.gpu) + 2 * sum(1 for seg in sched.gpu for v in seg.nodes if v in sched.host_consumed) + \
+                2 * sum(1 for seg in sched.gpu for m in pred[seg.nodes[0]] if sel[m] != GPU)
+            ev_pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+            for e in ev_pool + [ev0]:
+                e.record(stream)
             torch.cuda.synchronize(dev)
-            t_start = time.perf_counter()
-            ev0.record(stream)
+            ev_pool.reverse()
         seg_events = []
         xfer_events = []  # (src, dst, start_evt, end_evt, mb)
 
@@ -376,9 +393,9 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
             return hs_d[ld][s], (cs_d[ld][s] if lstm else None)
         return hs_h[ld][s], (cs_h[ld][s] if lstm else None)
 
-    def gpu_worker():
+    def gpu_worker():  # runs on the calling thread, inside the device / stream context
         try:
-            with torch.cuda.device(dev), torch.cuda.stream(stream):
+            if True:
                 for seg in sched.gpu:
                     ld, s0, s1 = seg.ld, seg.s0, seg.s1
                     l, d = divmod(ld, D)
@@ -389,7 +406,7 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
                             continue
                         _wait(ready[m], fail)
                         ml, md, mt, ms = cells[m]
-                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0, e1 = ev_pool.pop(), ev_pool.pop()
                         e0.record(stream)
                         if ml == l and md == d:  # state edge
                             hs_d[ld][ms].copy_(hs_h[ld][ms], non_blocking=True)
@@ -406,10 +423,10 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
                     inp = x_dev if l == 0 else act_d[l - 1]
                     h_prev, c_prev = state_slice(ld, s0 - 1, "d")
                     h_last, c_last = state_slice(ld, s1 - 1, "d")
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0, e1 = ev_pool.pop(), ev_pool.pop()
                     e0.record(stream)
-                    ex.run_cells(ld, s0, s1, inp, act_d[l], h_prev.contiguous(),
-                                 c_prev.contiguous() if lstm else None, h_last, c_last)
+                    ex.run_cells(ld, s0, s1, inp, act_d[l], h_prev, c_prev if lstm else None, h_last, c_last,
+                                 stream=stream)
                     e1.record(stream)
                     seg_events.append((seg, e0, e1))
                     # outputs that host cells read: D2H on the copy stream
@@ -418,7 +435,7 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
                             continue
                         vl, vd, vt, vs = cells[v]
                         copy_stream.wait_event(e1)
-                        c0e, c1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        c0e, c1e = ev_pool.pop(), ev_pool.pop()
                         c0e.record(copy_stream)
                         with torch.cuda.stream(copy_stream):
                             nbytes = 0
@@ -476,10 +493,20 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
     prev_switch = sys.getswitchinterval()
     sys.setswitchinterval(5e-5)
     tasks = [(host_worker, (c, q)) for c, q in sorted(sched.host.items())]
-    if uses_gpu:
-        tasks.append((gpu_worker, ()))
     pool = _worker_pool(len(tasks))
-    for fut in [pool.submit(fn, *args) for fn, args in tasks]:
+    if uses_gpu:
+        # the GPU queue runs on the calling thread (no hand-off before its
+        # first launch), inside its device / stream context entered before
+        # the clock starts
+        with torch.cuda.device(dev), torch.cuda.stream(stream):
+            t_start = time.perf_counter()
+            ev0.record(stream)
+            futs = [pool.submit(fn, *args) for fn, args in tasks]
+            gpu_worker()
+    else:
+        t_start = time.perf_counter()
+        futs = [pool.submit(fn, *args) for fn, args in tasks]
+    for fut in futs:
         fut.result()
     sys.setswitchinterval(prev_switch)
     if fail.exc is not None:
@@ -527,10 +554,13 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
         y = act_h[L - 1]
         hn = torch.stack([state_slice(ld, T - 1, "h")[0] for ld in range(LD)]).clone()
         cn = torch.stack([state_slice(ld, T - 1, "h")[1] for ld in range(LD)]).clone() if lstm else None
-    makespan = max([end_ms] + [sp.end for sp in spans])
+    # the reference's makespan (engine.py:408-415): last node end, or the end
+    # of a host-bound output transfer; the assembly above is in wall_ms only
+    makespan = max([sp.end for sp in spans] + [tr.end for tr in transfers if tr.dst < 0])
     spans.sort(key=lambda sp: (sp.start, sp.node))
     transfers.sort(key=lambda x: (x.start, x.src, x.dst))
-    return ExecResult(y, hn, cn, Trace(nodes=tuple(spans), transfers=tuple(transfers), makespan=makespan))
+    return ExecResult(y, hn, cn, Trace(nodes=tuple(spans), transfers=tuple(transfers), makespan=makespan),
+                      wall_ms=max(end_ms, makespan))
 
 
 # ----------------------------------------------------------------- profiler

@@ -604,18 +604,26 @@ class RNNExecutor:
         state = torch.empty((2, s.layers * s.dirs, s.batch, s.hidden), device=self.device)
         return xd, self.alloc_outputs(), state
 
-    def run_cells(self, ld: int, t0: int, t1: int, inp, out, h_prev, c_prev, h_last, c_last):
-        """Steps ``t0..t1-1`` (processing order) of layer-direction ``ld``."""
+    def run_cells(self, ld: int, t0: int, t1: int, inp, out, h_prev, c_prev, h_last, c_last, stream=None):
+        """Steps ``t0..t1-1`` (processing order) of layer-direction ``ld``, on
+        ``stream`` (a ``torch.cuda.Stream`` of this executor's device; default:
+        the device's current stream).  The hybrid executor passes its stream so
+        a segment's dispatch skips the device-context switch."""
         self._require_resident()
         ptr = lambda t: t.data_ptr() if t is not None else None
-        with torch.cuda.device(self.device):
-            stream = torch.cuda.current_stream(self.device)
-            _check(
-                self.lib,
-                "hs_rnn_run_cells",
-                self.lib.hs_rnn_run_cells(
-                    ctypes.byref(self.desc), self.packed.data_ptr(), ld, t0, t1, ptr(inp), ptr(out),
-                    ptr(h_prev), ptr(c_prev), ptr(h_last), ptr(c_last), self.workspace.data_ptr(),
-                    self.workspace.numel(), stream.cuda_stream,
-                ),
-            )
+        if stream is None:
+            with torch.cuda.device(self.device):
+                stream = torch.cuda.current_stream(self.device)
+        elif (self.device.index is not None and
+              (stream.device.index != self.device.index or torch.cuda.current_device() != self.device.index)):
+            raise ValueError(f"run_cells(stream=...) needs a stream of {self.device} and that device current "
+                             f"(got a stream on {stream.device}, current device {torch.cuda.current_device()})")
+        _check(
+            self.lib,
+            "hs_rnn_run_cells",
+            self.lib.hs_rnn_run_cells(
+                ctypes.byref(self.desc), self.packed.data_ptr(), ld, t0, t1, ptr(inp), ptr(out),
+                ptr(h_prev), ptr(c_prev), ptr(h_last), ptr(c_last), self.workspace.data_ptr(),
+                self.workspace.numel(), stream.cuda_stream,
+            ),
+        )

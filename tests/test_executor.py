@@ -126,6 +126,8 @@ def test_all_host_plan_matches_oracle(spec):
         assert err(res, ref) <= TOL
         assert sorted(s.node for s in res.trace.nodes) == list(range(g.n))
         assert res.trace.transfers == ()
+        # the reference's makespan: last node end (engine.py:408-415); wall_ms adds the assembly
+        assert res.trace.makespan == max(s.end for s in res.trace.nodes) <= res.wall_ms
         # each core runs its cells one at a time, in plan order
         pos = {v: i for i, v in enumerate(plan.order.seq)}
         for core in set(plan.cores):
@@ -209,6 +211,8 @@ def test_all_gpu_plan_is_fused_forward():
     y, hn, cn = ex.forward(x.to(ex.device))
     assert torch.equal(res.y, y) and torch.equal(res.hn, hn) and torch.equal(res.cn, cn)
     assert len(res.trace.nodes) == g.n and res.trace.makespan > 0
+    assert abs(res.trace.makespan - max(sp.end for sp in res.trace.nodes)) < 1e-9  # engine.py:408-415
+    assert res.wall_ms >= res.trace.makespan
 
 
 @pytest.mark.gpu

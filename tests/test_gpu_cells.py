@@ -70,6 +70,51 @@ def test_segments_on_tensor_cores_compose_to_the_forward(spec):
         assert float((cn - cn_f).abs().max()) <= 1e-6
 
 
+SMALL_SPECS = [
+    RNNSpec("lstm", 1, 128, 16, 1, algo="simt"),  # BASELINE c1 (auto resolves to this path)
+    RNNSpec("gru", 2, 64, 9, 4, dirs=2, algo="simt"),
+    RNNSpec("lstm", 2, 96, 7, 3, input=40, dirs=2, algo="simt"),
+]
+
+
+@pytest.mark.parametrize("spec", SMALL_SPECS, ids=[f"{s.cell}{s.layers}x{s.hidden}T{s.seq}B{s.batch}d{s.dirs}" for s in SMALL_SPECS])
+def test_segments_on_the_small_shape_kernel_compose_to_the_forward(spec):
+    """Shapes the fused forward runs on the small-shape cluster kernel run
+    their hybrid-plan segments on it too (one launch per segment, steps
+    s_base.. of the layer, reverse direction included): what profile_ops
+    timed for W[:, 0].  Same per-step arithmetic as the fused launch."""
+    w = init_weights(spec, 2)
+    x = make_input(spec, 3).cuda()
+    ex = RNNExecutor(spec, w)
+    assert ex.algo == "simt"
+    y_f, hn_f, cn_f = ex.forward(x)
+    T, B, H, D = spec.seq, spec.batch, spec.hidden, spec.dirs
+    inp = x
+    hn = torch.empty_like(hn_f)
+    cn = torch.empty_like(hn_f)
+    for l in range(spec.layers):
+        out = torch.zeros((T, B, D * H), device="cuda")
+        for d in range(D):
+            ld = l * D + d
+            h = torch.zeros((B, H), device="cuda")
+            c = torch.zeros((B, H), device="cuda")
+            for t0, t1 in ((0, 3), (3, T // 2 + 1), (T // 2 + 1, T)):
+                h2, c2 = torch.empty_like(h), torch.empty_like(c)
+                ex.run_cells(ld, t0, t1, inp, out, h, c if spec.cell == "lstm" else None, h2,
+                             c2 if spec.cell == "lstm" else None)
+                assert ex.last_launch_count() == 1  # the small-shape cluster kernel alone
+                h, c = h2, c2
+            hn[ld], cn[ld] = h, c
+        inp = out
+    torch.cuda.synchronize()
+    assert float((out - y_f).abs().max()) <= 1e-6
+    assert float((hn - hn_f).abs().max()) <= 1e-6
+    if spec.cell == "lstm":
+        assert float((cn - cn_f).abs().max()) <= 1e-6
+    ry, _rhn, _rcn = oracle(spec, w, x.cpu())
+    assert float(np.abs(out.cpu().double().numpy() - ry).max()) <= TOL
+
+
 @pytest.mark.parametrize("spec", TC_SPECS, ids=IDS)
 def test_hybrid_plans_on_tensor_core_segments(spec):
     g = grid_of(spec)
