@@ -3,7 +3,9 @@
 (B=64) with the dynamic next-layer K1, the layer-wave fused kernel at c3
 width, the W-streaming recurrence at c4 width (H=2048), the batch-sliced bf16
 path at c5 width, the host-buffer request stream (request overlap, async
-output drain) and two layer-pipeline stages (stream-ordered peer hand-off)."""
+output drain), two layer-pipeline stages (stream-ordered peer hand-off) and
+hybrid-plan GPU segments (hs_rnn_run_cells on the small-shape cluster kernel
+and on the tensor-core path, reverse direction included)."""
 import sys
 from pathlib import Path
 
@@ -55,3 +57,24 @@ if not only or "stage" in only:
                                    consumed_peer=consumed.data_ptr(), consumed_value=v1["consumed_value"], chunks=2))
     torch.cuda.synchronize()
     print("ok pipeline stages", flush=True)
+if not only or "segments" in only:
+    # hybrid-plan GPU segments: three segments per layer-direction
+    for spec in (RNNSpec("lstm", 2, 96, 7, 3, input=40, dirs=2, algo="simt"),
+                 RNNSpec("gru", 2, 256, 6, 8, dirs=2, algo="tc")):
+        ex = RNNExecutor(spec, init_weights(spec))
+        x = make_input(spec).cuda()
+        T, B, H, D = spec.seq, spec.batch, spec.hidden, spec.dirs
+        inp = x
+        for l in range(spec.layers):
+            out = torch.zeros((T, B, D * H), device="cuda")
+            for d in range(D):
+                h = torch.zeros((B, H), device="cuda")
+                c = torch.zeros((B, H), device="cuda")
+                for t0, t1 in ((0, 2), (2, 4), (4, T)):
+                    h2, c2 = torch.empty_like(h), torch.empty_like(c)
+                    lstm = spec.cell == "lstm"
+                    ex.run_cells(l * D + d, t0, t1, inp, out, h, c if lstm else None, h2, c2 if lstm else None)
+                    h, c = h2, c2
+            inp = out
+        torch.cuda.synchronize()
+        print("ok segments", spec.cell, ex.algo, flush=True)
