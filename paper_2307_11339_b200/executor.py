@@ -393,72 +393,74 @@ def _execute_hybrid(graph, plan, sched: Schedule, model, x, h0, c0) -> ExecResul
             return hs_d[ld][s], (cs_d[ld][s] if lstm else None)
         return hs_h[ld][s], (cs_h[ld][s] if lstm else None)
 
+    def take_ev():  # a pre-made timing event (a fresh one if the count was short)
+        return ev_pool.pop() if ev_pool else torch.cuda.Event(enable_timing=True)
+
     def gpu_worker():  # runs on the calling thread, inside the device / stream context
         try:
-            if True:
-                for seg in sched.gpu:
-                    ld, s0, s1 = seg.ld, seg.s0, seg.s1
-                    l, d = divmod(ld, D)
-                    first = seg.nodes[0]
-                    # host-produced inputs of the first node: wait, then H2D
-                    for m in pred[first]:
-                        if sel[m] == GPU:
-                            continue
-                        _wait(ready[m], fail)
-                        ml, md, mt, ms = cells[m]
-                        e0, e1 = ev_pool.pop(), ev_pool.pop()
-                        e0.record(stream)
-                        if ml == l and md == d:  # state edge
-                            hs_d[ld][ms].copy_(hs_h[ld][ms], non_blocking=True)
-                            nbytes = B * H * 4
-                            if lstm:
-                                cs_d[ld][ms].copy_(cs_h[ld][ms], non_blocking=True)
-                                nbytes *= 2
-                        else:  # layer-input edge
-                            sl = slice(md * H, (md + 1) * H)
-                            act_d[ml][mt, :, sl].copy_(act_h[ml][mt, :, sl], non_blocking=True)
-                            nbytes = B * H * 4
-                        e1.record(stream)
-                        xfer_events.append((m, first, e0, e1, nbytes / MB))
-                    inp = x_dev if l == 0 else act_d[l - 1]
-                    h_prev, c_prev = state_slice(ld, s0 - 1, "d")
-                    h_last, c_last = state_slice(ld, s1 - 1, "d")
-                    e0, e1 = ev_pool.pop(), ev_pool.pop()
+            for seg in sched.gpu:
+                ld, s0, s1 = seg.ld, seg.s0, seg.s1
+                l, d = divmod(ld, D)
+                first = seg.nodes[0]
+                # host-produced inputs of the first node: wait, then H2D
+                for m in pred[first]:
+                    if sel[m] == GPU:
+                        continue
+                    _wait(ready[m], fail)
+                    ml, md, mt, ms = cells[m]
+                    e0, e1 = take_ev(), take_ev()
                     e0.record(stream)
-                    ex.run_cells(ld, s0, s1, inp, act_d[l], h_prev, c_prev if lstm else None, h_last, c_last,
-                                 stream=stream)
+                    if ml == l and md == d:  # state edge
+                        hs_d[ld][ms].copy_(hs_h[ld][ms], non_blocking=True)
+                        nbytes = B * H * 4
+                        if lstm:
+                            cs_d[ld][ms].copy_(cs_h[ld][ms], non_blocking=True)
+                            nbytes *= 2
+                    else:  # layer-input edge
+                        sl = slice(md * H, (md + 1) * H)
+                        act_d[ml][mt, :, sl].copy_(act_h[ml][mt, :, sl], non_blocking=True)
+                        nbytes = B * H * 4
                     e1.record(stream)
-                    seg_events.append((seg, e0, e1))
-                    # outputs that host cells read: D2H on the copy stream
-                    for v in seg.nodes:
-                        if v not in sched.host_consumed:
-                            continue
-                        vl, vd, vt, vs = cells[v]
-                        copy_stream.wait_event(e1)
-                        c0e, c1e = ev_pool.pop(), ev_pool.pop()
-                        c0e.record(copy_stream)
-                        with torch.cuda.stream(copy_stream):
-                            nbytes = 0
-                            for w in succ[v]:
-                                if sel[w] == GPU:
-                                    continue
-                                wl, wd, _wt, _ws = cells[w]
-                                if wl == vl and wd == vd:
-                                    if vs != s1 - 1:
-                                        raise AssertionError("state edge leaves a GPU segment mid-way")
-                                    hs_h[ld][vs].copy_(hs_d[ld][vs], non_blocking=True)
+                    xfer_events.append((m, first, e0, e1, nbytes / MB))
+                inp = x_dev if l == 0 else act_d[l - 1]
+                h_prev, c_prev = state_slice(ld, s0 - 1, "d")
+                h_last, c_last = state_slice(ld, s1 - 1, "d")
+                e0, e1 = take_ev(), take_ev()
+                e0.record(stream)
+                ex.run_cells(ld, s0, s1, inp, act_d[l], h_prev, c_prev if lstm else None, h_last, c_last,
+                             stream=stream)
+                e1.record(stream)
+                seg_events.append((seg, e0, e1))
+                # outputs that host cells read: D2H on the copy stream
+                for v in seg.nodes:
+                    if v not in sched.host_consumed:
+                        continue
+                    vl, vd, vt, vs = cells[v]
+                    copy_stream.wait_event(e1)
+                    c0e, c1e = take_ev(), take_ev()
+                    c0e.record(copy_stream)
+                    with torch.cuda.stream(copy_stream):
+                        nbytes = 0
+                        for w in succ[v]:
+                            if sel[w] == GPU:
+                                continue
+                            wl, wd, _wt, _ws = cells[w]
+                            if wl == vl and wd == vd:
+                                if vs != s1 - 1:
+                                    raise AssertionError("state edge leaves a GPU segment mid-way")
+                                hs_h[ld][vs].copy_(hs_d[ld][vs], non_blocking=True)
+                                nbytes += B * H * 4
+                                if lstm:
+                                    cs_h[ld][vs].copy_(cs_d[ld][vs], non_blocking=True)
                                     nbytes += B * H * 4
-                                    if lstm:
-                                        cs_h[ld][vs].copy_(cs_d[ld][vs], non_blocking=True)
-                                        nbytes += B * H * 4
-                                else:
-                                    sl = slice(vd * H, (vd + 1) * H)
-                                    act_h[vl][vt, :, sl].copy_(act_d[vl][vt, :, sl], non_blocking=True)
-                                    nbytes += B * H * 4
-                        c1e.record(copy_stream)
-                        d2h_evt[v] = c1e
-                        xfer_events.append((v, -1, c0e, c1e, nbytes / MB))
-                        ready[v].set()
+                            else:
+                                sl = slice(vd * H, (vd + 1) * H)
+                                act_h[vl][vt, :, sl].copy_(act_d[vl][vt, :, sl], non_blocking=True)
+                                nbytes += B * H * 4
+                    c1e.record(copy_stream)
+                    d2h_evt[v] = c1e
+                    xfer_events.append((v, -1, c0e, c1e, nbytes / MB))
+                    ready[v].set()
         except BaseException as exc:  # surface in the caller
             fail.set(exc)
 
