@@ -656,7 +656,7 @@ def profile_ops(graph: Graph, model, k: int | None = None, reps: int = 5, b: flo
       ``reps``.  An all-GPU plan's modelled latency therefore equals the
       measured forward, and the split between cells follows
       the measured steps (e.g. the wavefront's pipeline fill).  Hybrid plans'
-      GPU segments run the same tensor-core kernels (``hs_rnn_run_cells``).
+      GPU segments run the fused forward's own kernels (``hs_rnn_run_cells``: tensor-core, or the small-shape cluster kernel).
       Needs an RNNExecutor; with a HostRNN the GPU column is the host column
       x 1e3 so no plan selects the GPU.
     * ``W[:, j]``, j = 1..k: host ms per cell with ``j`` cells running at once.
