@@ -6,8 +6,12 @@
 // W = W_hi + W_lo):  X_hi·W_hi + X_hi·W_lo + X_lo·W_hi, accumulated in f32 in
 // TMEM (≈16-bit operands; max-abs error ~1e-6 at the BASELINE configs, well
 // inside the 1e-4 budget — a single bf16 pass is ~5e-4).  bf16
-// mode runs the first pass only.  The passes are just a longer K loop over
-// (plane_a, plane_b) pairs, so the pipeline is a plain warp-specialised GEMM:
+// mode runs the first pass only.  The persistent and dynamic kernels issue
+// the three products per 64-wide K-block from ONE load of its four tiles
+// (X_hi, X_lo, W_hi, W_lo in a slot pair of the ring; ncu at c2: 158.6 ->
+// 153.2 us per layer, L2 throughput 56% -> 43%); the one-tile-per-CTA kernel
+// and HS_K1_FUSED3=0 run them pass-major, as a longer K loop over
+// (plane_a, plane_b) pairs.  The pipeline is a plain warp-specialised GEMM:
 //   warp 0   TMA producer (one elected lane), 4-stage smem ring, 128B swizzle
 //   warp 1   MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
 //   warp 2   TMEM allocator (BN f32 columns)
@@ -21,6 +25,27 @@ namespace tc {
 
 constexpr int GBM = 128;
 constexpr int GBK = 64;
+
+// K1 fused three-product K-blocks (f32 mode); HS_K1_FUSED3=0 selects the
+// pass-major loop (A/B).  Set per device by the host before the first K1.
+__constant__ int c_k1_fused3 = 1;
+__device__ __forceinline__ bool k1_fused3() { return c_k1_fused3 != 0; }
+
+// Fused three-product K-block (f32 mode): X_hi·W_hi + X_hi·W_lo + X_lo·W_hi of
+// one 64-wide K-block whose four tiles sit in a slot pair of the ring.
+__device__ __forceinline__ void mma_three_products(uint32_t acc, const __nv_bfloat16* ah, const __nv_bfloat16* al,
+                                                   const __nv_bfloat16* bh, const __nv_bfloat16* bl, uint32_t idesc,
+                                                   bool first) {
+#pragma unroll
+  for (int k = 0; k < GBK / 16; ++k) {
+    const uint64_t adh = ptx::sdesc_k_sw128(ah + k * 16), adl = ptx::sdesc_k_sw128(al + k * 16);
+    const uint64_t bdh = ptx::sdesc_k_sw128(bh + k * 16), bdl = ptx::sdesc_k_sw128(bl + k * 16);
+    ptx::mma_bf16_ss(acc, adh, bdh, idesc, !(first && k == 0));
+    ptx::mma_bf16_ss(acc, adh, bdl, idesc, 1);
+    ptx::mma_bf16_ss(acc, adl, bdh, idesc, 1);
+  }
+}
+
 // BN = 256: 4-stage ring, one CTA per SM.  BN = 128: 3-stage ring and two
 // CTAs per SM, so one CTA's epilogue overlaps the other's MMAs.
 template <int BN>
@@ -161,6 +186,9 @@ __global__ void __launch_bounds__(256, 1)
   GemmPSmem& sm = *reinterpret_cast<GemmPSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = K / GBK, nkb = npass * nk;
+  // f32 mode: the three products of a K-block from one load of its four tiles
+  // (X_hi, X_lo, W_hi, W_lo) instead of three passes re-loading X_hi and W_hi
+  const bool f3 = npass == 3 && k1_fused3();
   const int tiles_n = N / BN, tiles = ((M + GBM - 1) / GBM) * tiles_n;
   const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -188,6 +216,18 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < my_tiles; ++j) {
         const int t = blockIdx.x + j * gridDim.x;
         const int m0 = (t / tiles_n) * GBM, n0 = (t % tiles_n) * BN;
+        if (f3) {  // one super-stage (slot pair) per K-block: hi planes in slot 2p, lo planes in 2p+1
+          for (int kk = 0; kk < nk; ++kk) {
+            const int g = j * nk + kk, sp = g % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
+            if (g >= ST / 2) ptx::mbar_wait(&sm.empty[s0], ((g / (ST / 2)) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&sm.full[s0], 2 * (GBM + BN) * GBK * 2);
+            ptx::tma_load_3d(sm.a[s0], &tmA, &sm.full[s0], kk * GBK, m0, 0);
+            ptx::tma_load_3d(sm.b[s0], &tmB, &sm.full[s0], kk * GBK, n0, 0);
+            ptx::tma_load_3d(sm.a[s1], &tmA, &sm.full[s0], kk * GBK, m0, 1);
+            ptx::tma_load_3d(sm.b[s1], &tmB, &sm.full[s0], kk * GBK, n0, 1);
+          }
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           const int g = j * nkb + kb, st = g % ST;
           if (g >= ST) ptx::mbar_wait(&sm.empty[st], ((g / ST) - 1) & 1);
@@ -208,6 +248,17 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);  // epilogue drained it
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        if (f3) {
+          for (int kk = 0; kk < nk; ++kk) {
+            const int g = j * nk + kk, sp = g % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
+            ptx::mbar_wait(&sm.full[s0], (g / (ST / 2)) & 1);
+            ptx::tc_fence_after();
+            mma_three_products(acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
+            ptx::mma_commit(&sm.empty[s0]);
+          }
+          ptx::mma_commit(&sm.tmem_full[buf]);
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           const int g = j * nkb + kb, st = g % ST;
           ptx::mbar_wait(&sm.full[st], (g / ST) & 1);
@@ -333,6 +384,9 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
   // k-blocks of a tile of segment sg (passes x K/64); the ring position is a
   // running count because wave segments may differ in K
   auto nkb_of = [&](int sg) -> int { return g.npass * ((wave ? g.wK[sg] : g.K) / GBK); };
+  // f32 mode with an even ring of >= 4 slots: fused three-product K-blocks,
+  // one slot pair per K-block (see gemm_xproj_persistent)
+  const bool f3 = g.npass == 3 && ST >= 4 && k1_fused3();
   const int nseg = wave ? g.nseg : g.D;
   const int tiles_n = g.N / BN, per_m = nseg * tiles_n;
   const int tiles_m = (g.M + GBM - 1) / GBM;
@@ -404,6 +458,18 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
         const CUtensorMap* ta = &mp.a[wave ? sg : 0];
         const CUtensorMap* tb = &mp.b[sg];
         const int nkb = nkb_of(sg), nk = nkb / g.npass;
+        if (f3) {
+          for (int kk = 0; kk < nk; ++kk, ++gi) {
+            const int sp = gi % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
+            if (gi >= ST / 2) ptx::mbar_wait(&sm.empty[s0], ((gi / (ST / 2)) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&sm.full[s0], 2 * (GBM + BN) * GBK * 2);
+            ptx::tma_load_3d(sm.a[s0], ta, &sm.full[s0], kk * GBK, m0, 0);
+            ptx::tma_load_3d(sm.b[s0], tb, &sm.full[s0], kk * GBK, n0, 0);
+            ptx::tma_load_3d(sm.a[s1], ta, &sm.full[s0], kk * GBK, m0, 1);
+            ptx::tma_load_3d(sm.b[s1], tb, &sm.full[s0], kk * GBK, n0, 1);
+          }
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb, ++gi) {
           const int st = gi % ST;
           if (gi >= ST) ptx::mbar_wait(&sm.empty[st], ((gi / ST) - 1) & 1);
@@ -428,6 +494,17 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
         const int nkb = nkb_of((t % per_m) / tiles_n);
+        if (f3) {
+          for (int kk = 0; kk < nkb / 3; ++kk, ++gi) {
+            const int sp = gi % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
+            ptx::mbar_wait(&sm.full[s0], (gi / (ST / 2)) & 1);
+            ptx::tc_fence_after();
+            mma_three_products(acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
+            ptx::mma_commit(&sm.empty[s0]);
+          }
+          ptx::mma_commit(&sm.tmem_full[buf]);
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb, ++gi) {
           const int st = gi % ST;
           ptx::mbar_wait(&sm.full[st], (gi / ST) & 1);

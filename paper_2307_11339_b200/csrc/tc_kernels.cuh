@@ -289,6 +289,26 @@ inline int set_smem(K kernel, size_t bytes, std::string& err) {
   return 0;
 }
 
+// HS_K1_FUSED3=0 (A/B): the f32-mode K1 runs its three products pass-major
+// (three sweeps over K re-loading X_hi / W_hi) instead of fused per K-block.
+// The flag lives in each device's module constant; set once per device.
+inline int k1_mode_init(std::string& err) {
+  static const char* env = getenv("HS_K1_FUSED3");
+  if (!env || atoi(env) != 0) return 0;
+  static bool done_d[kMaxDev] = {};
+  bool& done = done_d[cur_device()];
+  if (!done) {
+    const int zero = 0;
+    cudaError_t e = cudaMemcpyToSymbol(c_k1_fused3, &zero, sizeof zero);
+    if (e != cudaSuccess) {
+      err = std::string("k1_mode_init: ") + cudaGetErrorString(e);
+      return 2;
+    }
+    done = true;
+  }
+  return 0;
+}
+
 // K1 on planes: A planes [2][M][K], W_ih planes [2][N][K]
 // (a_pstride: element distance between the A hi and lo planes; 0 = M*K)
 // persistent = false: one CTA per tile.  Required when the launch shares the
@@ -299,7 +319,8 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
                        int npass, cudaStream_t s, std::string& err, size_t a_pstride = 0, bool persistent = true) {
   CUtensorMap ta, tb;
   const int BN = gemm_bn(N);
-  int rc = make_map3(&ta, apl, K, M, 2, GBM, err, a_pstride);
+  int rc = k1_mode_init(err);
+  if (!rc) rc = make_map3(&ta, apl, K, M, 2, GBM, err, a_pstride);
   if (!rc) rc = make_map3(&tb, wpl, K, N, 2, BN, err);
   if (rc) return rc;
   dim3 grid(N / BN, (M + GBM - 1) / GBM);
@@ -353,7 +374,8 @@ inline int gemm_dyn_preload(std::string& err) {  // loads the module (lazy loadi
 inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
                            const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
   DynMaps mp;
-  int rc = make_map3(&mp.a[0], apl, ga.K, ga.M, 2, GBM, err, a_pstride);
+  int rc = k1_mode_init(err);
+  if (!rc) rc = make_map3(&mp.a[0], apl, ga.K, ga.M, 2, GBM, err, a_pstride);
   for (int d = 0; d < ga.D && !rc; ++d) rc = make_map3(&mp.b[d], wpl[d], ga.K, ga.N, 2, 256, err);
   if (rc) return rc;
   if ((rc = gemm_dyn_preload(err))) return rc;
@@ -373,7 +395,7 @@ inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __n
 inline int gemm_planes_wave(const __nv_bfloat16* const* apl, size_t a_pstride, const __nv_bfloat16* const* wpl,
                             const GemmDynArgs& ga, int grid, cudaStream_t s, std::string& err) {
   DynMaps mp;
-  int rc = 0;
+  int rc = k1_mode_init(err);
   for (int j = 0; j < ga.nseg && !rc; ++j) {
     rc = make_map3(&mp.a[j], apl[j], ga.K, ga.M, 2, GBM, err, a_pstride);
     if (!rc) rc = make_map3(&mp.b[j], wpl[j], ga.K, ga.N, 2, 256, err);

@@ -170,7 +170,7 @@ inline int launch_wave(int G, int NPL, const WavePlan& p, const __nv_bfloat16* c
   wa.nrec = L * RB * S;
   WaveMaps rm;
   DynMaps gm;
-  int rc = 0;
+  int rc = k1_mode_init(err);
   for (int l = 0; l < L && !rc; ++l) {
     TcRecurArgs& a = wa.rec.layer[l];
     a.S = S;
