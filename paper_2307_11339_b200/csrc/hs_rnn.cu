@@ -190,6 +190,20 @@ int small_cluster(const Dims& m) {
   return 0;
 }
 
+// K1 pass scheme of layer l (tc_gemm.cuh k1_idesc): bf16 mode 1; f32 mode 3
+// for layer 0 (the raw input: bf16 hi/lo X and W, three products) and 2 for
+// the hidden layers (X = h rounded to fp16 once, fp16 hi/lo row-scaled W:
+// the recurrence's own h·W_hh operand scheme, 2/3 of the tensor work).
+// Layer 0 keeps three products because its input has arbitrary range and
+// magnitude (one fp16 rounding of |x| ~ 1 inputs costs c_n 1.8e-4 at c2,
+// profiles/r02_k1_fp16_twopass.txt).  HS_K1_F16_HIDDEN=0: 3 everywhere (A/B).
+inline int k1_scheme(const Dims& m, int l) {
+  if (m.dtype == HS_DTYPE_BF16) return 1;
+  static const char* env = getenv("HS_K1_F16_HIDDEN");
+  if (env && atoi(env) == 0) return 3;
+  return l > 0 ? 2 : 3;
+}
+
 int pack_layout(const Dims& m, PackLayout* p) {
   if (m.L * m.D > 64) return fail(HS_ERR_UNSUPPORTED, "at most 64 layer-directions");
   size_t off = 0;
@@ -699,7 +713,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
   if (k1_before) {
     const LayerPack& lp = pl.ld[0];
     rc = gemm_planes(xpl, at<__nv_bfloat16>(packed, lp.tc), at<float>(packed, lp.bias_x), at<float>(ws, ww.xproj[0]),
-                     (int)TB, m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err);
+                     (int)TB, m.G * m.H, m.I, k1_scheme(m, 0), s, g_err);
     if (rc) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
   }
   {
@@ -720,7 +734,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
   WaveArgs wa{};
   wa.rec.L = m.L;
   GemmDynArgs ga{};
-  ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.H; ga.npass = NPL == 2 ? 3 : 1;
+  ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.H; ga.npass = k1_scheme(m, 1);
   ga.D = 1; ga.T = m.T; ga.B = m.B;
   ga.claim = at<unsigned int>(ws, ww.claim);
   ga.nseg = m.L - seg0;
@@ -738,7 +752,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
     const int Il = m.in_size(l);
     const LayerPack& lp = pl.ld[l];
     const __nv_bfloat16* wihp = at<__nv_bfloat16>(packed, lp.tc);
-    whh[l] = wihp + 2 * wih_plane_elems(m.G, m.H, Il);
+    whh[l] = whh_of(wihp, m.G, m.H, Il);
     TcRecurArgs& a = wa.rec.layer[l];
     a.H = m.H; a.B = m.B; a.Npad = pad16(m.B); a.T = m.T; a.D = 1; a.Bst = m.B;
     float* xp = at<float>(ws, ww.xproj[l]);
@@ -752,6 +766,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
     const bool lastl = l == m.L - 1;
     a.y = lastl ? y : nullptr;
     a.ypl = lastl ? nullptr : at<__nv_bfloat16>(ws, ww.ypl[l]);
+    a.ypl_f16 = !lastl && k1_scheme(m, l + 1) == 2;
     a.hbuf = at<uint16_t>(ws, ww.hbuf[l]);
     a.counters = at<unsigned int>(ws, ww.counters[l]);
     a.progress = at<unsigned int>(ws, ww.progress[l]);
@@ -766,6 +781,7 @@ int wave_layers(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const
       ga.bias[j] = at<float>(packed, lp.bias_x);
       ga.C[j] = xp;
       ga.wK[j] = Il;
+      ga.wnpass[j] = k1_scheme(m, l);
       ga.wprogress[j] = l == 0 ? nullptr : at<unsigned int>(ws, ww.progress[l - 1]);
       ga.wncta[j] = ncta;
       ga.wxready[j] = at<unsigned int>(ws, ww.xready[l]);
@@ -915,7 +931,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     // this xproj buffer are free then); it must NOT wait for s, which is still
     // running the previous forward's last recurrence
     if ((rc = join(ov->cs_in, gs))) return rc;
-    if ((rc = split_planes(x, xpl, TB, m.I, gs, g_err, TB * m.I))) return rc;
+    if ((rc = split_planes(x, xpl, TB, m.I, false, gs, g_err, TB * m.I))) return rc;
     HS_CUDA(cudaEventRecord(x_free, gs));  // x consumed: the next upload into it may start
     unsigned int* claim = reinterpret_cast<unsigned int*>(tcws + tw.claim);
     HS_CUDA(cudaMemsetAsync(claim, 0, sizeof(unsigned int), gs));
@@ -926,7 +942,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       ga.bias[d] = at<float>(packed, pl.ld[d].bias_x);
       ga.C[d] = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
     }
-    ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.I; ga.npass = NPL == 2 ? 3 : 1;
+    ga.M = (int)TB; ga.N = m.G * m.H; ga.K = m.I; ga.npass = k1_scheme(m, 0);
     ga.D = m.D; ga.T = m.T; ga.B = m.B;
     ga.claim = claim;
     ga.progress = nullptr;  // rows are all present
@@ -962,12 +978,12 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const size_t r0 = (size_t)t0 * m.B, nr = (size_t)(t1 - t0) * m.B;
       HS_CUDA(cudaStreamWaitEvent(s, ev_in[k], 0));
       HS_CUDA(cudaEventDestroy(ev_in[k]));
-      if ((rc = split_planes(x + r0 * m.I, xpl + r0 * m.I, nr, m.I, s, g_err, TB * m.I))) return rc;
+      if ((rc = split_planes(x + r0 * m.I, xpl + r0 * m.I, nr, m.I, false, s, g_err, TB * m.I))) return rc;
       for (int d = 0; d < m.D; ++d) {
         const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, pl.ld[d].tc);
         float* xp = at<float>(ws, wl.xproj) + (size_t)d * TB * m.G * m.H;
         rc = gemm_planes(xpl + r0 * m.I, wih, at<float>(packed, pl.ld[d].bias_x), xp + r0 * m.G * m.H, (int)nr,
-                         m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err, TB * m.I);
+                         m.G * m.H, m.I, k1_scheme(m, 0), s, g_err, TB * m.I);
         if (rc) return rc;
       }
     }
@@ -989,7 +1005,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, pl.ld[0].tc);
       float* xp = at<float>(ws, wl.xproj);
       rc = gemm_planes(xin + r0 * m.I, wih, at<float>(packed, pl.ld[0].bias_x), xp + r0 * m.G * m.H, (int)nr,
-                       m.G * m.H, m.I, NPL == 2 ? 3 : 1, s, g_err, TB * m.I);
+                       m.G * m.H, m.I, k1_scheme(m, 0), s, g_err, TB * m.I);
       if (rc) return rc;
     }
     if (lk->consumed_peer) {  // the slot may be refilled by the previous stage
@@ -997,7 +1013,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       if (r != CUDA_SUCCESS) return fail(HS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
     }
   } else {
-    rc = split_planes(x, xpl, TB, m.I, s, g_err);
+    rc = split_planes(x, xpl, TB, m.I, false, s, g_err);
     if (rc) return rc;
   }
   if (wp.S) return wave_layers(m, di, pl, packed, x, h0, c0, y, hn, cn, ws, wl, s, gs, ov, chunked_in, xreq_ok, wp, evs, nev,
@@ -1045,10 +1061,10 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       const int ld = l * m.D + d;
       const LayerPack& lp = pl.ld[ld];
       const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
-      whh[d] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
+      whh[d] = whh_of(wih, m.G, m.H, Il);
       float* xp = xpl_l + (size_t)d * TB * m.G * m.H;
       if (k1_now) {
-        rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
+        rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp, (int)TB, m.G * m.H, Il, k1_scheme(m, l), s, g_err);
         if (rc) return rc;
       }
       a.xproj[d] = xp;
@@ -1062,6 +1078,9 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
     const bool last = l == m.L - 1;
     a.y = last ? y : nullptr;
     a.ypl = last && !peer_out ? nullptr : xpl;  // a stage's last layer writes the next stage's input planes
+    // the next layer's K1 operand: fp16 for a hidden layer of this executor;
+    // bf16 hi/lo for the next stage (its layer 0 runs the three-product scheme)
+    a.ypl_f16 = !last && k1_scheme(m, l + 1) == 2;
     a.hbuf = reinterpret_cast<uint16_t*>(hbuf);
     a.counters = counters;
     a.stamps = g_stamps ? g_stamps + (size_t)l * m.D * (m.T + 1) : nullptr;
@@ -1123,7 +1142,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
       for (int d = 0; d < m.D; ++d) {
         const LayerPack& lp = pl.ld[l * m.D + d];
         rc = gemm_planes(xpl, at<__nv_bfloat16>(packed, lp.tc), at<float>(packed, lp.bias_x), const_cast<float*>(a.xproj[d]),
-                         (int)TB, m.G * m.H, Il, NPL == 2 ? 3 : 1, s, g_err);
+                         (int)TB, m.G * m.H, Il, k1_scheme(m, l), s, g_err);
         if (rc) return rc;
       }
     }
@@ -1146,7 +1165,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         xga.bias[d] = at<float>(packed, lp.bias_x);
         xga.C[d] = xpl_l + (size_t)d * TB * m.G * m.H;
       }
-      xga.M = (int)TB; xga.N = m.G * m.H; xga.K = Il; xga.npass = NPL == 2 ? 3 : 1;
+      xga.M = (int)TB; xga.N = m.G * m.H; xga.K = Il; xga.npass = k1_scheme(m, l);
       xga.D = m.D; xga.T = m.T; xga.B = m.B;
       xga.xready = xready;
       if (PA > 0) {
@@ -1262,7 +1281,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
         ga.bias[d] = at<float>(packed, lpn.bias_x);
         ga.C[d] = xpb[(l + 1) & 1] + (size_t)d * TB * m.G * m.H;
       }
-      ga.M = (int)TB; ga.N = m.G * m.H; ga.K = In; ga.npass = NPL == 2 ? 3 : 1;
+      ga.M = (int)TB; ga.N = m.G * m.H; ga.K = In; ga.npass = k1_scheme(m, l + 1);
       ga.D = m.D; ga.T = m.T; ga.B = m.B;
       ga.claim = claim;
       ga.progress = a.progress;
@@ -1285,7 +1304,7 @@ int tc_forward(const Dims& m, const DeviceInfo& di, const PackLayout& pl, const 
           const __nv_bfloat16* wihn = at<__nv_bfloat16>(packed, lpn.tc);
           float* xpn = xpb[(l + 1) & 1] + (size_t)d * TB * m.G * m.H;
           rc = gemm_planes(xpl + r0 * In, wihn, at<float>(packed, lpn.bias_x), xpn + r0 * m.G * m.H, (int)nr,
-                           m.G * m.H, In, NPL == 2 ? 3 : 1, gs, g_err, TB * In, /*persistent=*/false);
+                           m.G * m.H, In, k1_scheme(m, l + 1), gs, g_err, TB * In, /*persistent=*/false);
           if (rc) return rc;
         }
       }
@@ -1502,9 +1521,9 @@ int tc_run_cells(const Dims& m, const DeviceInfo& di, const PackLayout& pl, cons
   float* xp = at<float>(ws, wl.xproj) + (size_t)d * m.T * m.B * GH;
   const __nv_bfloat16* wih = at<__nv_bfloat16>(packed, lp.tc);
   int rc;
-  if ((rc = split_planes(in + (size_t)tlo * m.B * Il, xpl, rows, Il, s, g_err))) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
+  if ((rc = split_planes(in + (size_t)tlo * m.B * Il, xpl, rows, Il, k1_scheme(m, l) == 2, s, g_err))) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
   if ((rc = gemm_planes(xpl, wih, at<float>(packed, lp.bias_x), xp + (size_t)tlo * m.B * GH, (int)rows, GH, Il,
-                        NPL == 2 ? 3 : 1, s, g_err)))
+                        k1_scheme(m, l), s, g_err)))
     return fail(HS_ERR_CUDA, "%s", g_err.c_str());
   {
     ZeroList zl{};
@@ -1532,7 +1551,7 @@ int tc_run_cells(const Dims& m, const DeviceInfo& di, const PackLayout& pl, cons
   a.counters = reinterpret_cast<unsigned int*>(tcws + tw.counters);
   a.l2_hints = kL2HintW | kL2HintStream;
   const __nv_bfloat16* whh[2];
-  whh[0] = whh[1] = wih + 2 * wih_plane_elems(m.G, m.H, Il);
+  whh[0] = whh[1] = whh_of(wih, m.G, m.H, Il);
   rc = recurrence_layer(m.G, NPL, whh, a, di.sms, s, g_err);
   if (rc == 3) return -1;
   if (rc) return fail(HS_ERR_CUDA, "%s", g_err.c_str());
@@ -1641,7 +1660,7 @@ int hs_rnn_pack_weights(const hs_rnn_desc* desc, const void* const* w_ih, const 
       HS_CUDA(cudaGetLastError());
       if (lp.tc) {
         rc = hs::tc::pack_layer(m.G, m.H, m.in_size(l), static_cast<const float*>(w_ih[ld]), static_cast<const float*>(w_hh[ld]),
-                                at<unsigned char>(packed, lp.tc), m.dtype != HS_DTYPE_BF16, s, g_err);
+                                at<unsigned char>(packed, lp.tc), m.dtype != HS_DTYPE_BF16, k1_scheme(m, l) == 2, s, g_err);
         if (rc) return rc;
       }
     }

@@ -211,6 +211,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor: kind::f16, A=B=fp16, D=f32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B
 // (64 bf16), 8-row atoms of 1024 B (SBO), atoms 1024-B aligned.
 __device__ __forceinline__ uint64_t sdesc_k_sw128(const void* smem) {

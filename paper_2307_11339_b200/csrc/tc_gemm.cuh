@@ -2,16 +2,17 @@
 //
 //   XP[M, N] = X[M, K] · W_ih[N, K]ᵀ + bias[N]      M = T·B, N = G·H, K = I_l
 //
-// f32 mode runs three bf16 passes over split operands (x = x_hi + x_lo,
-// W = W_hi + W_lo):  X_hi·W_hi + X_hi·W_lo + X_lo·W_hi, accumulated in f32 in
-// TMEM (≈16-bit operands; max-abs error ~1e-6 at the BASELINE configs, well
-// inside the 1e-4 budget — a single bf16 pass is ~5e-4).  bf16
-// mode runs the first pass only.  The persistent and dynamic kernels issue
-// the three products per 64-wide K-block from ONE load of its four tiles
-// (X_hi, X_lo, W_hi, W_lo in a slot pair of the ring; ncu at c2: 158.6 ->
-// 153.2 us per layer, L2 throughput 56% -> 43%); the one-tile-per-CTA kernel
-// and HS_K1_FUSED3=0 run them pass-major, as a longer K loop over
-// (plane_a, plane_b) pairs.  The pipeline is a plain warp-specialised GEMM:
+// Pass schemes (npass): 3 = f32 mode for layer 0 (the raw input): bf16
+// hi/lo X and W, X_hi·W_hi + X_hi·W_lo + X_lo·W_hi accumulated in f32 in TMEM
+// (≈16-bit operands); 2 = f32 mode for the hidden layers: X = h rounded to
+// fp16 once times fp16 hi/lo of the row-scaled W_ih (X·W_hi + X·W_lo, the
+// recurrence's own h·W_hh scheme; the epilogue applies the row scales);
+// 1 = bf16 mode, one product.  The f32-mode kernels issue the products of a
+// 64-wide K-block from one load of its tiles (a slot pair of the ring) in the
+// same order everywhere (load_kblock_fused / mma_kblock_fused); bf16 mode and
+// HS_K1_FUSED3=0 run the passes as a longer K loop over (plane_a, plane_b)
+// pairs.  ncu at c2 (scheme 3): 158.6 -> 153.2 us per layer fused, L2
+// throughput 56% -> 43%.  The pipeline is a plain warp-specialised GEMM:
 //   warp 0   TMA producer (one elected lane), 4-stage smem ring, 128B swizzle
 //   warp 1   MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
 //   warp 2   TMEM allocator (BN f32 columns)
@@ -26,23 +27,57 @@ namespace tc {
 constexpr int GBM = 128;
 constexpr int GBK = 64;
 
-// K1 fused three-product K-blocks (f32 mode); HS_K1_FUSED3=0 selects the
-// pass-major loop (A/B).  Set per device by the host before the first K1.
+// K1 fused K-blocks (f32 mode, pass schemes 2 and 3); HS_K1_FUSED3=0 selects
+// the pass-major loop (A/B).  Set per device by the host before the first K1.
 __constant__ int c_k1_fused3 = 1;
 __device__ __forceinline__ bool k1_fused3() { return c_k1_fused3 != 0; }
 
-// Fused three-product K-block (f32 mode): X_hi·W_hi + X_hi·W_lo + X_lo·W_hi of
-// one 64-wide K-block whose four tiles sit in a slot pair of the ring.
-__device__ __forceinline__ void mma_three_products(uint32_t acc, const __nv_bfloat16* ah, const __nv_bfloat16* al,
-                                                   const __nv_bfloat16* bh, const __nv_bfloat16* bl, uint32_t idesc,
-                                                   bool first) {
+// Pass schemes (npass): 3 = f32 mode, bf16 hi/lo X and W, three products
+// (layer 0: the raw input); 2 = f32 mode for hidden-state inputs, X rounded
+// to fp16 once (plane 0) times fp16 hi/lo W of the row-scaled weights —
+// exactly the recurrence's own h·W_hh operand scheme — with the row scales
+// applied in the epilogue; 1 = bf16 mode, one bf16 product.
+__device__ __forceinline__ uint32_t k1_idesc(int npass, int BN) {
+  return npass == 2 ? ptx::idesc_f16_f32(GBM, BN) : ptx::idesc_bf16_f32(GBM, BN);
+}
+// accumulator columns of W_ih rows scaled by 2^e -> times 2^-e
+__device__ __forceinline__ void apply_scale(float (&v)[32], const float* __restrict__ sc) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 4) {
+    const float4 f = *reinterpret_cast<const float4*>(sc + j);
+    v[j] *= f.x;
+    v[j + 1] *= f.y;
+    v[j + 2] *= f.z;
+    v[j + 3] *= f.w;
+  }
+}
+
+// Fused K-block (pass schemes 2 and 3): every product of one 64-wide K-block
+// from ONE load of its tiles, staged in a slot pair (s0, s1) of the ring:
+//   a[s0] = X plane 0, b[s0] = W hi, b[s1] = W lo, a[s1] = X lo (scheme 3)
+// products per K=16 step: X0·W_hi, X0·W_lo (+ X_lo·W_hi for scheme 3).
+// Every kernel issues them in this order, so a layer's K1 is bit-identical
+// whichever kernel (persistent, one tile per CTA, dynamic, wave) runs it.
+template <int BN>
+__device__ __forceinline__ void load_kblock_fused(int np, __nv_bfloat16* a0, __nv_bfloat16* a1, __nv_bfloat16* b0,
+                                                  __nv_bfloat16* b1, const CUtensorMap* ta, const CUtensorMap* tb,
+                                                  uint64_t* bar, int kk, int m0, int n0) {
+  ptx::mbar_arrive_expect_tx(bar, (uint32_t)((np == 3 ? 2 * (GBM + BN) : GBM + 2 * BN) * GBK * 2));
+  ptx::tma_load_3d(a0, ta, bar, kk * GBK, m0, 0);
+  ptx::tma_load_3d(b0, tb, bar, kk * GBK, n0, 0);
+  ptx::tma_load_3d(b1, tb, bar, kk * GBK, n0, 1);
+  if (np == 3) ptx::tma_load_3d(a1, ta, bar, kk * GBK, m0, 1);
+}
+__device__ __forceinline__ void mma_kblock_fused(int np, uint32_t acc, const __nv_bfloat16* a0, const __nv_bfloat16* a1,
+                                                 const __nv_bfloat16* b0, const __nv_bfloat16* b1, uint32_t idesc,
+                                                 bool first) {
 #pragma unroll
   for (int k = 0; k < GBK / 16; ++k) {
-    const uint64_t adh = ptx::sdesc_k_sw128(ah + k * 16), adl = ptx::sdesc_k_sw128(al + k * 16);
-    const uint64_t bdh = ptx::sdesc_k_sw128(bh + k * 16), bdl = ptx::sdesc_k_sw128(bl + k * 16);
-    ptx::mma_bf16_ss(acc, adh, bdh, idesc, !(first && k == 0));
-    ptx::mma_bf16_ss(acc, adh, bdl, idesc, 1);
-    ptx::mma_bf16_ss(acc, adl, bdh, idesc, 1);
+    const uint64_t ad0 = ptx::sdesc_k_sw128(a0 + k * 16), bd0 = ptx::sdesc_k_sw128(b0 + k * 16);
+    const uint64_t bd1 = ptx::sdesc_k_sw128(b1 + k * 16);
+    ptx::mma_bf16_ss(acc, ad0, bd0, idesc, !(first && k == 0));
+    ptx::mma_bf16_ss(acc, ad0, bd1, idesc, 1);
+    if (np == 3) ptx::mma_bf16_ss(acc, ptx::sdesc_k_sw128(a1 + k * 16), bd0, idesc, 1);
   }
 }
 
@@ -75,7 +110,8 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 template <int BN>
 __global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
     gemm_xproj_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int npass) {
+                      const float* __restrict__ bias, const float* __restrict__ scale, float* __restrict__ C, int M,
+                      int N, int K, int npass) {
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -83,6 +119,7 @@ __global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
   const int nk = K / GBK;
   const int nkb = npass * nk;
   constexpr int GSTAGES = gemm_stages<BN>();
+  const bool fz = npass >= 2 && k1_fused3();  // fused K-blocks in slot pairs (GSTAGES / 2 of them)
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
@@ -102,7 +139,12 @@ __global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
 
   if (warp == 0) {
     if (ptx::elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kk = 0; fz && kk < nk; ++kk) {
+        const int s0 = 2 * (kk % (GSTAGES / 2)), s1 = s0 + 1;
+        if (kk >= GSTAGES / 2) ptx::mbar_wait(&sm.empty[s0], ((kk / (GSTAGES / 2)) - 1) & 1);
+        load_kblock_fused<BN>(npass, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], &tmA, &tmB, &sm.full[s0], kk, m0, n0);
+      }
+      for (int kb = 0; !fz && kb < nkb; ++kb) {
         const int st = kb % GSTAGES;
         if (kb >= GSTAGES) ptx::mbar_wait(&sm.empty[st], ((kb / GSTAGES) - 1) & 1);
         const int pass = kb / nk, kk = kb % nk;
@@ -115,8 +157,15 @@ __global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
     __syncwarp();
   } else if (warp == 1) {
     if (ptx::elect_one()) {
-      const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
-      for (int kb = 0; kb < nkb; ++kb) {
+      const uint32_t idesc = k1_idesc(npass, BN);
+      for (int kk = 0; fz && kk < nk; ++kk) {
+        const int s0 = 2 * (kk % (GSTAGES / 2)), s1 = s0 + 1;
+        ptx::mbar_wait(&sm.full[s0], (kk / (GSTAGES / 2)) & 1);
+        ptx::tc_fence_after();
+        mma_kblock_fused(npass, tmem, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
+        ptx::mma_commit(&sm.empty[s0]);
+      }
+      for (int kb = 0; !fz && kb < nkb; ++kb) {
         const int st = kb % GSTAGES;
         ptx::mbar_wait(&sm.full[st], (kb / GSTAGES) & 1);
         ptx::tc_fence_after();
@@ -143,6 +192,7 @@ __global__ void __launch_bounds__(256, BN == 256 ? 1 : 2)
       if (row < M) {
         const int n = n0 + c * 32;
         float* dst = C + (size_t)row * N + n;
+        if (scale) apply_scale(v, scale + n);
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const float4 bb = *reinterpret_cast<const float4*>(bias + n + j);
@@ -180,7 +230,8 @@ constexpr size_t gemm_p_smem_bytes() { return sizeof(GemmPSmem) + 1024; }
 
 __global__ void __launch_bounds__(256, 1)
     gemm_xproj_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int npass) {
+                          const float* __restrict__ bias, const float* __restrict__ scale, float* __restrict__ C,
+                          int M, int N, int K, int npass) {
   constexpr int BN = 256, ST = GemmPSmem::ST;
   extern __shared__ uint8_t smem_raw[];
   GemmPSmem& sm = *reinterpret_cast<GemmPSmem*>(align1024(smem_raw));
@@ -188,7 +239,7 @@ __global__ void __launch_bounds__(256, 1)
   const int nk = K / GBK, nkb = npass * nk;
   // f32 mode: the three products of a K-block from one load of its four tiles
   // (X_hi, X_lo, W_hi, W_lo) instead of three passes re-loading X_hi and W_hi
-  const bool f3 = npass == 3 && k1_fused3();
+  const bool f3 = npass >= 2 && k1_fused3();
   const int tiles_n = N / BN, tiles = ((M + GBM - 1) / GBM) * tiles_n;
   const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -220,11 +271,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < nk; ++kk) {
             const int g = j * nk + kk, sp = g % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
             if (g >= ST / 2) ptx::mbar_wait(&sm.empty[s0], ((g / (ST / 2)) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&sm.full[s0], 2 * (GBM + BN) * GBK * 2);
-            ptx::tma_load_3d(sm.a[s0], &tmA, &sm.full[s0], kk * GBK, m0, 0);
-            ptx::tma_load_3d(sm.b[s0], &tmB, &sm.full[s0], kk * GBK, n0, 0);
-            ptx::tma_load_3d(sm.a[s1], &tmA, &sm.full[s0], kk * GBK, m0, 1);
-            ptx::tma_load_3d(sm.b[s1], &tmB, &sm.full[s0], kk * GBK, n0, 1);
+            load_kblock_fused<BN>(npass, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], &tmA, &tmB, &sm.full[s0], kk, m0, n0);
           }
           continue;
         }
@@ -242,7 +289,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (ptx::elect_one()) {
-      const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
+      const uint32_t idesc = k1_idesc(npass, BN);
       for (int j = 0; j < my_tiles; ++j) {
         const int buf = j & 1;
         if (j >= 2) ptx::mbar_wait(&sm.tmem_empty[buf], ((j >> 1) - 1) & 1);  // epilogue drained it
@@ -253,7 +300,7 @@ __global__ void __launch_bounds__(256, 1)
             const int g = j * nk + kk, sp = g % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
             ptx::mbar_wait(&sm.full[s0], (g / (ST / 2)) & 1);
             ptx::tc_fence_after();
-            mma_three_products(acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
+            mma_kblock_fused(npass, acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
             ptx::mma_commit(&sm.empty[s0]);
           }
           ptx::mma_commit(&sm.tmem_full[buf]);
@@ -291,6 +338,7 @@ __global__ void __launch_bounds__(256, 1)
         if (row < M) {
           const int n = n0 + c * 32;
           float* dst = C + (size_t)row * N + n;
+          if (scale) apply_scale(v, scale + n);
 #pragma unroll
           for (int q = 0; q < 32; q += 4) {
             const float4 bb = *reinterpret_cast<const float4*>(bias + n + q);
@@ -329,7 +377,8 @@ constexpr int kMaxSeg = 8;  // segments of a dynamic K1 launch (directions, or t
 struct GemmDynArgs {
   const float* bias[kMaxSeg];      // per segment [N]
   float* C[kMaxSeg];               // per segment [M, N]
-  int M, N, K, npass, D, T, B;
+  const float* scale[kMaxSeg];     // per segment [N] W_ih row inverse scales (pass scheme 2), else nullptr
+  int M, N, K, npass, D, T, B;     // npass: pass scheme (see k1_idesc); wave mode: per segment in wnpass
   unsigned int* claim;             // zeroed before launch
   const unsigned int* progress;    // [T] CTAs of the recurrence that finished step s
   unsigned int ncta;               // progress[s] value meaning "step s complete everywhere"
@@ -344,6 +393,7 @@ struct GemmDynArgs {
   // claimed tile depends on (m' <= m of segment j-1) was claimed before it.
   int nseg, lag;
   int wK[kMaxSeg];                 // wave mode: contraction length of each segment (layer input width)
+  int wnpass[kMaxSeg];             // wave mode: pass scheme of each segment
   const unsigned int* wprogress[kMaxSeg];
   unsigned int wncta[kMaxSeg];
   unsigned int* wxready[kMaxSeg];
@@ -383,11 +433,14 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
   const bool wave = g.nseg > 0;
   // k-blocks of a tile of segment sg (passes x K/64); the ring position is a
   // running count because wave segments may differ in K
-  auto nkb_of = [&](int sg) -> int { return g.npass * ((wave ? g.wK[sg] : g.K) / GBK); };
-  // f32 mode with an even ring of >= 4 slots: fused three-product K-blocks,
-  // one slot pair per K-block (see gemm_xproj_persistent)
-  const bool f3 = g.npass == 3 && ST >= 4 && k1_fused3();
+  auto np_of = [&](int sg) -> int { return wave ? g.wnpass[sg] : g.npass; };  // pass scheme of segment sg
+  auto nkb_of = [&](int sg) -> int { return np_of(sg) * ((wave ? g.wK[sg] : g.K) / GBK); };
   const int nseg = wave ? g.nseg : g.D;
+  // f32-mode schemes (2, 3): fused K-blocks, one slot pair each (ST / 2
+  // pairs; one, unpipelined, for ST = 2), in the same product order as the
+  // other K1 kernels.  bf16 mode (1) runs pass-major.
+  bool f3 = k1_fused3();
+  for (int j = 0; j < nseg; ++j) f3 = f3 && np_of(j) >= 2;
   const int tiles_n = g.N / BN, per_m = nseg * tiles_n;
   const int tiles_m = (g.M + GBM - 1) / GBM;
   const int tiles_all = tiles_m * per_m;
@@ -457,16 +510,12 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
         }
         const CUtensorMap* ta = &mp.a[wave ? sg : 0];
         const CUtensorMap* tb = &mp.b[sg];
-        const int nkb = nkb_of(sg), nk = nkb / g.npass;
+        const int nkb = nkb_of(sg), nk = nkb / np_of(sg);
         if (f3) {
           for (int kk = 0; kk < nk; ++kk, ++gi) {
             const int sp = gi % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
             if (gi >= ST / 2) ptx::mbar_wait(&sm.empty[s0], ((gi / (ST / 2)) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&sm.full[s0], 2 * (GBM + BN) * GBK * 2);
-            ptx::tma_load_3d(sm.a[s0], ta, &sm.full[s0], kk * GBK, m0, 0);
-            ptx::tma_load_3d(sm.b[s0], tb, &sm.full[s0], kk * GBK, n0, 0);
-            ptx::tma_load_3d(sm.a[s1], ta, &sm.full[s0], kk * GBK, m0, 1);
-            ptx::tma_load_3d(sm.b[s1], tb, &sm.full[s0], kk * GBK, n0, 1);
+            load_kblock_fused<BN>(np_of(sg), sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], ta, tb, &sm.full[s0], kk, m0, n0);
           }
           continue;
         }
@@ -484,7 +533,6 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
     __syncwarp();
   } else if (warp == 1) {
     if (ptx::elect_one()) {
-      const uint32_t idesc = ptx::idesc_bf16_f32(GBM, BN);
       int gi = 0;  // ring position
       for (int j = 0;; ++j) {
         const int t = next_tile(j);
@@ -494,12 +542,14 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
         const int nkb = nkb_of((t % per_m) / tiles_n);
+        const uint32_t idesc = k1_idesc(np_of((t % per_m) / tiles_n), BN);
         if (f3) {
-          for (int kk = 0; kk < nkb / 3; ++kk, ++gi) {
+          const int np = np_of((t % per_m) / tiles_n);
+          for (int kk = 0; kk < nkb / np; ++kk, ++gi) {
             const int sp = gi % (ST / 2), s0 = 2 * sp, s1 = s0 + 1;
             ptx::mbar_wait(&sm.full[s0], (gi / (ST / 2)) & 1);
             ptx::tc_fence_after();
-            mma_three_products(acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
+            mma_kblock_fused(np, acc, sm.a[s0], sm.a[s1], sm.b[s0], sm.b[s1], idesc, kk == 0);
             ptx::mma_commit(&sm.empty[s0]);
           }
           ptx::mma_commit(&sm.tmem_full[buf]);
@@ -529,6 +579,7 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
       const int mt = t / per_m, sg = (t % per_m) / tiles_n, n0 = (t % tiles_n) * BN;
       const int m0 = mt * GBM;
       const float* __restrict__ bias = g.bias[sg];
+      const float* __restrict__ scale = g.scale[sg];
       float* __restrict__ C = g.C[sg];
       unsigned int* xr = wave ? g.wxready[sg] : g.xready;
       const int buf = j % NACC;
@@ -542,6 +593,7 @@ __device__ __forceinline__ void gemm_dyn_body(const DynMaps& mp, const GemmDynAr
         if (row < g.M) {
           const int n = n0 + c * 32;
           float* dst = C + (size_t)row * g.N + n;
+          if (scale) apply_scale(v, scale + n);
 #pragma unroll
           for (int q = 0; q < 32; q += 4) {
             const float4 bb = *reinterpret_cast<const float4*>(bias + n + q);
@@ -573,15 +625,22 @@ __global__ void __launch_bounds__(256, 1) gemm_xproj_dyn(const __grid_constant__
   gemm_dyn_body(mp, g, smem_raw);
 }
 
-// fp32 [rows, cols] (row stride ld) -> bf16 planes [2][rows][cols]; the lo
-// plane starts `pstride` elements after the hi plane (pstride = 0: rows*cols)
+// fp32 [rows, cols] (row stride ld) -> the K1 A operand planes [2][rows][cols]:
+// f16 = 1 (pass scheme 2, hidden-state inputs): fp16(x) in plane 0 only;
+// else bf16 hi/lo, the lo plane `pstride` elements after the hi plane
+// (pstride = 0: rows*cols)
 __global__ void split_planes_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, size_t rows, int cols,
-                                    int ld, size_t pstride) {
+                                    int ld, size_t pstride, int f16) {
   const size_t total = rows * (size_t)cols;
   for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; i < total; i += (size_t)gridDim.x * blockDim.x * 4) {
     const size_t r = i / cols;
     const int c = (int)(i % cols);
     const float4 v = *reinterpret_cast<const float4*>(x + r * ld + c);
+    if (f16) {
+      __align__(8) __half h4[4] = {__float2half_rn(v.x), __float2half_rn(v.y), __float2half_rn(v.z), __float2half_rn(v.w)};
+      *reinterpret_cast<uint2*>(out + i) = *reinterpret_cast<uint2*>(h4);
+      continue;
+    }
     const float f[4] = {v.x, v.y, v.z, v.w};
     __align__(8) __nv_bfloat16 hi[4], lo[4];
 #pragma unroll

@@ -98,18 +98,32 @@ inline int gemm_bn(int N) {
   return N % 256 == 0 ? 256 : 128;
 }
 
-// packed planes per layer-direction: W_ih [2][G*H][I] bf16, W_hh row-block packed [2][H/32*128][H] bf16
+// packed planes per layer-direction:
+//   W_ih [2][G*H][I] 16-bit hi/lo planes — bf16 for pass scheme 3 / 1 (layer
+//        0, bf16 mode), fp16 of the row-scaled weights for scheme 2 (hidden
+//        layers in f32 mode) — then their per-row inverse scales [G*H] f32
+//        (ones for bf16 planes), padded to 256 B;
+//   W_hh row-block packed [2][H/32*128][H] 16-bit planes, then their per-row
+//        inverse scales [H/32*128] f32.
 inline size_t wih_plane_elems(int G, int H, int I) { return (size_t)G * H * I; }
 inline size_t whh_plane_elems(int H) { return (size_t)(H / 32) * 128 * H; }
-// + per-row power-of-two scales of the fp16 W_hh planes ([H/32*128] f32)
+inline size_t wih_scale_bytes(int N) { return ((size_t)N * 4 + 255) / 256 * 256; }
 inline size_t packed_bytes(int G, int H, int I) {
   if (H % 32) return 0;
-  return 2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)) + 4 * (size_t)(H / 32) * 128;
+  return 2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)) + wih_scale_bytes(G * H) + 4 * (size_t)(H / 32) * 128;
 }
-
+// per-row inverse scales of the W_ih planes starting at `wih` ([2][N][K])
+inline const float* wih_scales(const void* wih, int N, int K) {
+  return reinterpret_cast<const float*>(static_cast<const unsigned char*>(wih) + 2 * 2 * (size_t)N * K);
+}
+// the W_hh planes of the layer whose W_ih planes start at `wih`
+inline const __nv_bfloat16* whh_of(const __nv_bfloat16* wih, int G, int H, int I) {
+  return reinterpret_cast<const __nv_bfloat16*>(reinterpret_cast<const unsigned char*>(wih) +
+                                                2 * 2 * wih_plane_elems(G, H, I) + wih_scale_bytes(G * H));
+}
 inline float* whh_scales(void* packed_layer, int G, int H, int I) {
   return reinterpret_cast<float*>(static_cast<unsigned char*>(packed_layer) +
-                                  2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)));
+                                  2 * 2 * (wih_plane_elems(G, H, I) + whh_plane_elems(H)) + wih_scale_bytes(G * H));
 }
 
 __global__ void fill_ones_kernel(float* p, int n) {
@@ -167,20 +181,51 @@ __global__ void whh_row_scale_kernel(const float* __restrict__ w_hh, float* __re
   }
 }
 
-// W_ih: bf16 hi/lo planes (K1 GEMM).  W_hh: fp16 hi/lo planes of the row-
-// scaled weights (f32 mode, whh_f16) or bf16 (bf16 mode uses plane 0 only),
-// row-block packed.
+// Per W_ih row (pass scheme 2): the same power-of-two scaling as W_hh's, so
+// the fp16 lo plane stays normal.  One warp per row.
+__global__ void wih_row_scale_kernel(const float* __restrict__ w_ih, float* __restrict__ inv_scale, int N, int K) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < N; r += (gridDim.x * blockDim.x) >> 5) {
+    float m = 0.f;
+    for (int k = lane; k < K; k += 32) m = fmaxf(m, fabsf(w_ih[(size_t)r * K + k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      int e = 0;
+      if (m > 0.f) {
+        int ex;
+        frexpf(m, &ex);
+        e = 14 - ex;
+        e = e > 60 ? 60 : e < -60 ? -60 : e;
+      }
+      inv_scale[r] = ldexpf(1.f, -e);
+    }
+  }
+}
+
+// W_ih: bf16 hi/lo planes, or (wih_f16, pass scheme 2) fp16 hi/lo planes of
+// the row-scaled weights.  W_hh: fp16 hi/lo planes of the row-scaled weights
+// (f32 mode, whh_f16) or bf16 (bf16 mode uses plane 0 only), row-block packed.
 __global__ void pack_tc_kernel(const float* __restrict__ w_ih, const float* __restrict__ w_hh,
                                __nv_bfloat16* __restrict__ wih_pl, __nv_bfloat16* __restrict__ whh_pl, int G, int H,
-                               int I, int whh_f16, const float* __restrict__ inv_scale) {
+                               int I, int whh_f16, const float* __restrict__ inv_scale, int wih_f16,
+                               const float* __restrict__ wih_inv_scale) {
   const size_t n_ih = (size_t)G * H * I;
   const size_t n_hh = (size_t)(H / 32) * 128 * H;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_ih; i += stride) {
-    __nv_bfloat16 hi, lo;
-    ptx::split_bf16(w_ih[i], hi, lo);
-    wih_pl[i] = hi;
-    wih_pl[n_ih + i] = lo;
+    if (wih_f16) {
+      const float vs = w_ih[i] / wih_inv_scale[i / I];  // exact: power of two
+      const __half hi = __float2half_rn(vs);
+      const __half lo = __float2half_rn(vs - __half2float(hi));
+      reinterpret_cast<uint16_t*>(wih_pl)[i] = __half_as_ushort(hi);
+      reinterpret_cast<uint16_t*>(wih_pl)[n_ih + i] = __half_as_ushort(lo);
+    } else {
+      __nv_bfloat16 hi, lo;
+      ptx::split_bf16(w_ih[i], hi, lo);
+      wih_pl[i] = hi;
+      wih_pl[n_ih + i] = lo;
+    }
   }
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_hh; i += stride) {
     const int k = (int)(i % H);
@@ -202,16 +247,21 @@ __global__ void pack_tc_kernel(const float* __restrict__ w_ih, const float* __re
   }
 }
 
+// wih_f16: pack W_ih for pass scheme 2 (a hidden layer's K1 in f32 mode)
 inline int pack_layer(int G, int H, int I, const float* w_ih, const float* w_hh, unsigned char* dst, bool whh_f16,
-                      cudaStream_t s, std::string& err) {
+                      bool wih_f16, cudaStream_t s, std::string& err) {
   __nv_bfloat16* wih = reinterpret_cast<__nv_bfloat16*>(dst);
-  __nv_bfloat16* whh = wih + 2 * wih_plane_elems(G, H, I);
+  __nv_bfloat16* whh = const_cast<__nv_bfloat16*>(whh_of(wih, G, H, I));
   float* inv_scale = whh_scales(dst, G, H, I);
+  float* wih_inv = const_cast<float*>(wih_scales(wih, G * H, I));
   whh_row_scale_kernel<<<148, 256, 0, s>>>(w_hh, inv_scale, G, H);
   if (!whh_f16) {  // bf16 mode: unscaled
     fill_ones_kernel<<<16, 256, 0, s>>>(inv_scale, (H / 32) * 128);
   }
-  pack_tc_kernel<<<592, 256, 0, s>>>(w_ih, w_hh, wih, whh, G, H, I, whh_f16 ? 1 : 0, inv_scale);
+  if (wih_f16) wih_row_scale_kernel<<<148, 256, 0, s>>>(w_ih, wih_inv, G * H, I);
+  else fill_ones_kernel<<<16, 256, 0, s>>>(wih_inv, G * H);
+  pack_tc_kernel<<<592, 256, 0, s>>>(w_ih, w_hh, wih, whh, G, H, I, whh_f16 ? 1 : 0, inv_scale, wih_f16 ? 1 : 0,
+                                     wih_inv);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("pack_tc_kernel: ") + cudaGetErrorString(e);
@@ -324,6 +374,7 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
   if (!rc) rc = make_map3(&tb, wpl, K, N, 2, BN, err);
   if (rc) return rc;
   dim3 grid(N / BN, (M + GBM - 1) / GBM);
+  const float* scale = npass == 2 ? wih_scales(wpl, N, K) : nullptr;  // pass scheme 2: row-scaled W_ih
   cudaError_t e;
   static const char* np_env = getenv("HS_GEMM_NONPERSISTENT");  // A/B runs
   if (BN == 256 && persistent && !np_env) {
@@ -337,17 +388,17 @@ inline int gemm_planes(const __nv_bfloat16* apl, const __nv_bfloat16* wpl, const
     }
     const int sms = sms_d[dev];
     const int tiles = (int)(grid.x * grid.y);
-    gemm_xproj_persistent<<<tiles < sms ? tiles : sms, 256, gemm_p_smem_bytes(), s>>>(ta, tb, bias, C, M, N, K, npass);
+    gemm_xproj_persistent<<<tiles < sms ? tiles : sms, 256, gemm_p_smem_bytes(), s>>>(ta, tb, bias, scale, C, M, N, K, npass);
   } else if (BN == 256) {
     static bool init_d[kMaxDev] = {};
   bool& init = init_d[cur_device()];
     if (!init) { if ((rc = set_smem(gemm_xproj_kernel<256>, gemm_smem_bytes<256>(), err))) return rc; init = true; }
-    gemm_xproj_kernel<256><<<grid, 256, gemm_smem_bytes<256>(), s>>>(ta, tb, bias, C, M, N, K, npass);
+    gemm_xproj_kernel<256><<<grid, 256, gemm_smem_bytes<256>(), s>>>(ta, tb, bias, scale, C, M, N, K, npass);
   } else {
     static bool init_d[kMaxDev] = {};
   bool& init = init_d[cur_device()];
     if (!init) { if ((rc = set_smem(gemm_xproj_kernel<128>, gemm_smem_bytes<128>(), err))) return rc; init = true; }
-    gemm_xproj_kernel<128><<<grid, 256, gemm_smem_bytes<128>(), s>>>(ta, tb, bias, C, M, N, K, npass);
+    gemm_xproj_kernel<128><<<grid, 256, gemm_smem_bytes<128>(), s>>>(ta, tb, bias, scale, C, M, N, K, npass);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -379,7 +430,9 @@ inline int gemm_planes_dyn(const __nv_bfloat16* apl, size_t a_pstride, const __n
   for (int d = 0; d < ga.D && !rc; ++d) rc = make_map3(&mp.b[d], wpl[d], ga.K, ga.N, 2, 256, err);
   if (rc) return rc;
   if ((rc = gemm_dyn_preload(err))) return rc;
-  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, ga);
+  GemmDynArgs g = ga;
+  for (int d = 0; d < ga.D; ++d) g.scale[d] = ga.npass == 2 ? wih_scales(wpl[d], ga.N, ga.K) : nullptr;
+  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("gemm_xproj_dyn launch: ") + cudaGetErrorString(e);
@@ -402,7 +455,9 @@ inline int gemm_planes_wave(const __nv_bfloat16* const* apl, size_t a_pstride, c
   }
   if (rc) return rc;
   if ((rc = gemm_dyn_preload(err))) return rc;
-  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, ga);
+  GemmDynArgs g = ga;
+  for (int j = 0; j < ga.nseg; ++j) g.scale[j] = g.wnpass[j] == 2 ? wih_scales(wpl[j], ga.N, ga.K) : nullptr;
+  gemm_xproj_dyn<<<grid, 256, gemm_d_smem_bytes(), s>>>(mp, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("gemm_xproj_dyn (wave) launch: ") + cudaGetErrorString(e);
@@ -412,13 +467,14 @@ inline int gemm_planes_wave(const __nv_bfloat16* const* apl, size_t a_pstride, c
   return 0;
 }
 
-inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int cols, cudaStream_t s, std::string& err,
-                        size_t pstride = 0) {
+// f16: pass scheme 2's single fp16 plane (hidden-state inputs); else bf16 hi/lo
+inline int split_planes(const float* x, __nv_bfloat16* out, size_t rows, int cols, bool f16, cudaStream_t s,
+                        std::string& err, size_t pstride = 0) {
   const size_t total = rows * cols;
   int blocks = (int)((total / 4 + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  split_planes_kernel<<<blocks, 256, 0, s>>>(x, out, rows, cols, cols, pstride);
+  split_planes_kernel<<<blocks, 256, 0, s>>>(x, out, rows, cols, cols, pstride, f16 ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("split_planes_kernel: ") + cudaGetErrorString(e);

@@ -41,7 +41,8 @@ struct TcRecurArgs {
   float* hn[2];                 // per dir [B][H]
   float* cn[2];
   float* y;                     // [T][B][D*H] f32, or nullptr
-  __nv_bfloat16* ypl;           // [2][T*B][D*H] bf16 planes for the next layer's K1, or nullptr
+  __nv_bfloat16* ypl;           // [2][T*B][D*H] planes for the next layer's K1, or nullptr
+  int ypl_f16;                  // 1: fp16(h) in plane 0 only (next K1 on pass scheme 2), 0: bf16 hi/lo
   uint16_t* hbuf;               // [3][D][Npad][H] h_{t-1} operand: fp16 (f32 mode) / bf16 (bf16 mode)
   unsigned int* counters;       // [D][S]
   unsigned long long* trace;    // optional [grid][kTraceSteps][16] %globaltimer stamps (debug)
@@ -232,10 +233,7 @@ __device__ __forceinline__ void cluster_wait() {
 constexpr int kRecurThreads = 256;  // + one W-producer warp in the streaming variant
 constexpr int kEpiThreads = 256;
 
-// tcgen05 instruction descriptor, kind::f16 with fp16 A/B and f32 D
-__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
-  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
+using ptx::idesc_f16_f32;  // tcgen05 instruction descriptor, kind::f16 with fp16 A/B and f32 D
 
 // The streamed h_{t-1} MMA operand.  f32 mode (NPL = 2 W_hh planes): fp16,
 // 11 significant bits, exact range for |h| < 1; W_hh is carried as fp16
@@ -650,10 +648,14 @@ __device__ __forceinline__ void recur_tc_body(const CUtensorMap& tmW0, const CUt
         else a.y[yidx] = hv;
       }
       if (a.ypl) {
-        __nv_bfloat16 hi, lo;
-        ptx::split_bf16(hv, hi, lo);
-        a.ypl[yidx] = hi;
-        a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
+        if (a.ypl_f16) {  // a hidden layer's K1 input: fp16(h), the recurrence's own h operand
+          reinterpret_cast<uint16_t*>(a.ypl)[yidx] = __half_as_ushort(__float2half_rn(hv));
+        } else {
+          __nv_bfloat16 hi, lo;
+          ptx::split_bf16(hv, hi, lo);
+          a.ypl[yidx] = hi;
+          a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
+        }
       }
       if (last) {
         a.hn[d][(size_t)b * H + unit] = hv;

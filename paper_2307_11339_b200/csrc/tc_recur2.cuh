@@ -363,10 +363,14 @@ __global__ void __launch_bounds__(256, 1)
       const size_t yidx = ((size_t)t * a.Bst + brow0 + b) * D * H + (size_t)d * H + unit;
       if (a.y) a.y[yidx] = hv;
       if (a.ypl) {
-        __nv_bfloat16 hi, lo;
-        ptx::split_bf16(hv, hi, lo);
-        a.ypl[yidx] = hi;
-        a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
+        if (a.ypl_f16) {  // a hidden layer's K1 input: fp16(h), the recurrence's own h operand
+          reinterpret_cast<uint16_t*>(a.ypl)[yidx] = __half_as_ushort(__float2half_rn(hv));
+        } else {
+          __nv_bfloat16 hi, lo;
+          ptx::split_bf16(hv, hi, lo);
+          a.ypl[yidx] = hi;
+          a.ypl[(size_t)T * a.Bst * D * H + yidx] = lo;
+        }
       }
       if (last) {
         a.hn[d][(size_t)(brow0 + b) * H + unit] = hv;

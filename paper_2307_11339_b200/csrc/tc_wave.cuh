@@ -182,6 +182,7 @@ inline int launch_wave(int G, int NPL, const WavePlan& p, const __nv_bfloat16* c
   for (int j = 0; j < ga.nseg && !rc; ++j) {  // K1 segments (apl / a_pstride / wih indexed by segment)
     rc = make_map3(&gm.a[j], apl[j], ga.wK[j], ga.M, 2, GBM, err, a_pstride[j]);
     if (!rc) rc = make_map3(&gm.b[j], wih[j], ga.wK[j], ga.N, 2, 256, err);
+    ga.scale[j] = ga.wnpass[j] == 2 ? wih_scales(wih[j], ga.N, ga.wK[j]) : nullptr;  // pass scheme 2: row-scaled W_ih
   }
   if (rc) return rc;
   const size_t smem = wave_smem(G, H, a0.B, S, NPL, p.per_sm);
